@@ -1,0 +1,141 @@
+/*
+ * rhseg_b200.h -- C ABI of librhseg_b200.so, the sm_100a RHSEG hot path.
+ *
+ * Plain C: pointers, sizes and status codes; no torch or C++ types cross the
+ * boundary. Every entry point returns RHSEG_OK (0) or an RHSEG_E_* status and
+ * leaves a thread-local message in rhseg_last_error(). No C++ exception ever
+ * crosses the boundary. There is no CPU fallback: without a usable sm_100a
+ * device every compute entry point returns RHSEG_E_CUDA.
+ *
+ * The reference (rhseg, pure Python + numba) has no FFI of its own; the seams it
+ * exposes for this path, and which these entry points replace, are:
+ *
+ *   B3 kernel seam  rhseg/_kernels.py:31-33  scan_adjacent(row_start, row_stop, counts,
+ *                   sums, indptr, indices, out_d, out_j)           -> rhseg_scan_adjacent
+ *                   rhseg/_kernels.py:62-65  scan_nonadjacent(row_start, row_stop,
+ *                   col_tile, ...)                                  -> rhseg_scan_nonadjacent
+ *                   (looked up as module attributes by engine._scan, engine.py:213-218)
+ *   B2 engine seam  rhseg/engine.py:345-371  hseg_run(graph, params, strategy, ...)
+ *                                                                    -> rhseg_hseg_graph
+ *   B1 executor     rhseg/recursive.py:179-209 executor.execute(image, params, strategy,
+ *                   profile) -> RhsegResult; rhseg_run recursive.py:212-223
+ *                                                    -> rhseg_run_device / rhseg_run_host
+ *                   + rhseg_result_* accessors for the RhsegResult fields
+ *                   (recursive.py:62-92: section_logs, root_initial, root_hierarchy,
+ *                   graph, labels, converged_early).
+ *
+ * Arithmetic contract: fp64, IEEE div/sqrt, no FMA, ascending-band accumulation,
+ * strict-< / lexicographic (d, min id, max id) tie-breaks -- merge logs, dissimilarities
+ * and labels are bit-identical to the reference CPU path.
+ */
+#ifndef RHSEG_B200_H
+#define RHSEG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RHSEG_ABI_VERSION 1
+
+#define RHSEG_OK 0
+#define RHSEG_E_INVALID 1     /* ValueError in the reference (engine.py:37-42, recursive.py:41-47) */
+#define RHSEG_E_INDIVISIBLE 2 /* errors.IndivisibleImage (sections.py:61-65) */
+#define RHSEG_E_CUDA 3        /* CUDA failure / no sm_100a device */
+#define RHSEG_E_TOO_LARGE 4   /* section exceeds the device limits (R0 > 16384 regions) */
+#define RHSEG_E_STATE 5       /* no result available / wrong call order */
+
+typedef struct rhseg_ctx rhseg_ctx;
+
+/* RhsegParams + HsegParams (recursive.py:30-59, engine.py:29-42). */
+typedef struct {
+    double spectral_weight;         /* w in [0, 1] */
+    int32_t target_regions;         /* >= 1; the root's stopping count */
+    int32_t section_target_regions; /* >= 1; every section above the root (0 = target) */
+    int32_t levels;                 /* >= 1 recursion levels */
+    int32_t connectivity;           /* 4 or 8 */
+    int32_t measure;                /* 0 = "sqrt-bsmse" (the only reference measure, dissim.py:45) */
+    int32_t cluster;                /* 0 = auto; else CTAs per section in {1,2,4,8,16} */
+} rhseg_params;
+
+typedef struct {
+    int64_t n_records;              /* merge records over all sections (log order) */
+    int64_t spectral_pairs;         /* reference-equivalent sum_steps (R(R-1)/2 - E), w > 0 */
+    int32_t n_sections;             /* sections over all levels */
+    int32_t levels, edge, bands;
+    int32_t root_idspace;           /* region id space of the root section */
+    int32_t root_initial_regions;   /* live regions of root_initial */
+    int32_t root_regions;           /* live regions after the root HSEG */
+    int32_t converged_early;        /* any section converged early (recursive.py:208) */
+    float device_ms;                /* device time of the last run (CUDA events) */
+    float pad_;
+} rhseg_result_info;
+
+int rhseg_abi_version(void);
+const char *rhseg_last_error(void);
+
+int rhseg_ctx_create(int device, rhseg_ctx **out);
+int rhseg_ctx_destroy(rhseg_ctx *ctx);
+
+/* ---- B1: full RHSEG (SequentialExecutor.execute, recursive.py:173-209) ----------- */
+/* d_samples: DEVICE pointer, float32 BSQ [bands][edge][edge] (image.py:12-52).
+ * stream: a cudaStream_t (NULL = legacy default). Results stay in the context. */
+int rhseg_run_device(rhseg_ctx *ctx, const float *d_samples, int32_t edge, int32_t bands,
+                     const rhseg_params *params, void *stream);
+/* Same from a HOST cube (pinned or pageable): H2D, run, D2H of the merge log (SoA,
+ * capacity edge*edge records each) and dense labels (edge*edge). Any output
+ * pointer may be NULL. */
+int rhseg_run_host(rhseg_ctx *ctx, const float *h_samples, int32_t edge, int32_t bands,
+                   const rhseg_params *params, void *stream, int32_t *log_survivor,
+                   int32_t *log_absorbed, double *log_dissim, uint8_t *log_kind,
+                   int32_t *labels, rhseg_result_info *info);
+
+int rhseg_result_info_get(rhseg_ctx *ctx, rhseg_result_info *info);
+/* Sections in log order (level L..1, row-major, recursive.py:95-104): n_sections entries. */
+int rhseg_result_sections(rhseg_ctx *ctx, int32_t *level, int32_t *row, int32_t *col,
+                          int64_t *offset, int64_t *count);
+/* Flat merge log, n_records entries each (host buffers). */
+int rhseg_result_log(rhseg_ctx *ctx, int32_t *survivor, int32_t *absorbed, double *dissim,
+                     uint8_t *kind);
+/* labels: dense, first row-major occurrence (graph.py:267-281); assignment: root ids. */
+int rhseg_result_labels(rhseg_ctx *ctx, int32_t *labels, int32_t *assignment);
+/* Root graph state, which = 0: root_initial (pre-root-HSEG, recursive.py:166-167),
+ * which = 1: final. counts[idspace] (0 = dead), sums[idspace][bands] f64,
+ * adjacency bitset[idspace][ceil(idspace/32)] u32, assignment[edge*edge]. */
+int rhseg_result_root(rhseg_ctx *ctx, int32_t which, int64_t *counts, double *sums,
+                      uint32_t *adjacency, int32_t *assignment);
+
+/* ---- B2: hseg_run on one region graph (engine.py:345-371) ---------------------- */
+/* Dense ascending-id graph as built by engine.snapshot (engine.py:167-191): counts[n]
+ * f64, sums[n][nbands] f64 row-major, CSR indptr[n+1]/indices int64 (host). Writes up
+ * to n-1 records; *n_records receives the count. */
+int rhseg_hseg_graph(rhseg_ctx *ctx, int64_t n, int64_t nbands, const double *counts,
+                     const double *sums, const int64_t *indptr, const int64_t *indices,
+                     double spectral_weight, int64_t target_regions, int32_t cluster,
+                     int32_t *log_survivor, int32_t *log_absorbed, double *log_dissim,
+                     uint8_t *log_kind, int64_t *n_records, int32_t *converged_early);
+
+/* ---- B3: per-row best-partner tables (_kernels.py:31-115), HOST buffers --------- */
+/* Rows [row_start, row_stop) of out_d/out_j are written, nothing else. n = rows of
+ * counts/sums; nbands = columns of sums. Reentrant (serialised internally). */
+int rhseg_scan_adjacent(int64_t row_start, int64_t row_stop, int64_t n, int64_t nbands,
+                        const double *counts, const double *sums, const int64_t *indptr,
+                        const int64_t *indices, double *out_d, int64_t *out_j);
+int rhseg_scan_nonadjacent(int64_t row_start, int64_t row_stop, int64_t col_tile, int64_t n,
+                           int64_t nbands, const double *counts, const double *sums,
+                           const int64_t *indptr, const int64_t *indices, double *out_d,
+                           int64_t *out_j);
+
+/* ---- measurement helpers ------------------------------------------------------ */
+/* Per-kernel device time of the last run: [0] leaf/graph init, [1] all-pairs D init,
+ * [2] merge loops, [3] stitch+resolve+labels (ms, CUDA events on the run stream). */
+int rhseg_result_phase_ms(rhseg_ctx *ctx, float *ms4);
+/* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure
+ * sub/mul/add loop over the whole GPU (roofline denominator). */
+int rhseg_fp64_peak(rhseg_ctx *ctx, double *ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,535 @@
+// hseg_kernels.cu -- the HSEG region-growing hot path on sm_100a.
+//
+// Reference semantics being replaced (rhseg, read-only at /root/reference/pkg/src):
+//   engine.py:309-342  hseg_step   (snapshot -> adjacent scan -> spectral scan -> rule -> merge)
+//   engine.py:345-371  hseg_run    (loop while live_count > target)
+//   _kernels.py:31-115 scan_adjacent / scan_nonadjacent (per-row best partner, fp64)
+//   graph.py:229-264   merge_regions (smaller id survives, sums add, adjacency union)
+//
+// B200 design (not a translation): the reference rebuilds both best-pair tables from
+// scratch every step, O(R^2 B). Here every section keeps, resident in HBM/L2,
+//   * an exact fp64 dissimilarity matrix D (all live pairs when w > 0, adjacent pairs
+//     when w = 0), filled once by the tiled all-pairs kernel `dinit_dense_kernel`;
+//   * per-row cached best partners for both stages (shared memory of the owning CTA).
+// A merge (a, b) only changes pairs that touch a or b, so each step recomputes the
+// single row a (R x B fp64 ops, bit-identical to the reference's op order), offers
+// (d(i, a), a) to every row i, and rescans from D only the rows whose cached partner
+// was a or b. Because the per-row caches always equal the reference's per-row table
+// entries and the global pick is the same lexicographic (d, min id, max id) minimum,
+// the merge sequence, dissimilarities and labels are bit-identical to hseg_run.
+//
+// One thread-block cluster (C CTAs, 1 <= C <= 16) owns one section and loops over all
+// of its merges without returning to the host: CTA r owns rows [r*Rs, (r+1)*Rs). The
+// single cross-CTA exchange per step is a 64-byte slot per CTA read through DSMEM after
+// one barrier.cluster (double-buffered by step parity).
+#include <cuda_runtime.h>
+
+#include "rhseg_batch.h"
+#include "rhseg_device.cuh"
+
+namespace rhseg {
+
+// ===========================================================================
+// 1. All-pairs D initialisation (the spectral-clustering all-pairs stage).
+//    64x64 pair tiles, 256 threads, 4x4 register blocking, bands staged through
+//    shared memory in ascending chunks (per-pair accumulation stays sequential in
+//    b, so blocking never changes a bit). FP64-pipe bound: 3 DP ops per pair-band.
+// ===========================================================================
+constexpr int kTile = 64;
+constexpr int kKB = 16;
+
+__global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) {
+    const int sec = bt.sec0 + blockIdx.y;
+    const int R0 = bt.R0[sec];
+    const int nt = (R0 + kTile - 1) / kTile;
+    int t = blockIdx.x;
+    if (t >= nt * (nt + 1) / 2) return;
+    int ti = 0;
+    while (t >= nt - ti) { t -= nt - ti; ++ti; }
+    const int tj = ti + t;
+    const int i0 = ti * kTile, j0 = tj * kTile;
+    const int B = bt.B, Rp = bt.Rp;
+    const double* __restrict__ mu = bt.mu + sec * bt.mu_stride();
+    double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    const uint32_t* __restrict__ cnt = bt.count + (size_t)sec * Rp;
+
+    // band staging (sA, sB) and the transpose tile (sT) share one buffer: sT is
+    // only touched after the last band chunk's trailing __syncthreads().
+    __shared__ double smraw[kTile * (kTile + 1)];
+    double (*sA)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw);
+    double (*sB)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw + kKB * kTile);
+    double (*sT)[kTile + 1] = reinterpret_cast<double (*)[kTile + 1]>(smraw);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+
+    for (int k0 = 0; k0 < B; k0 += kKB) {
+        const int kn = min(kKB, B - k0);
+        for (int e = threadIdx.x; e < kKB * kTile; e += kThreads) {
+            const int kk = e / kTile, r = e % kTile;
+            const bool in = kk < kn;
+            sA[kk][r] = in ? mu[(size_t)(k0 + kk) * Rp + i0 + r] : 0.0;
+            sB[kk][r] = in ? mu[(size_t)(k0 + kk) * Rp + j0 + r] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kn; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = sA[kk][ty + 16 * q];
+                b[q] = sB[kk][tx + 16 * q];
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[p][q] = bsmse_step(acc[p][q], a[p], b[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int i = i0 + ty + 16 * p;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + tx + 16 * q;
+            double d = 0.0;
+            if (i < R0 && j < R0) {
+                d = bsmse_finish((double)cnt[i], (double)cnt[j], acc[p][q]);
+                D[(size_t)i * Rp + j] = d;
+            }
+            sT[ty + 16 * p][tx + 16 * q] = d;
+        }
+    }
+    if (ti == tj) return;  // diagonal tile already holds both orders (d is bitwise symmetric)
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
+        const int r = e / kTile, c = e % kTile;  // output row j0+r, column i0+c
+        if (j0 + r < R0 && i0 + c < R0) D[(size_t)(j0 + r) * Rp + i0 + c] = sT[c][r];
+    }
+}
+
+// w = 0: only adjacent pairs are ever read (engine.py:326 skips the spectral stage),
+// so D is filled on the adjacency graph only. One thread per row.
+__global__ void __launch_bounds__(kThreads) dinit_sparse_kernel(SectionBatch bt) {
+    const int sec = bt.sec0 + blockIdx.y;
+    const int R0 = bt.R0[sec];
+    const int i = blockIdx.x * kThreads + threadIdx.x;
+    if (i >= R0) return;
+    const int B = bt.B, Rp = bt.Rp, W = bt.W;
+    const uint32_t* cnt = bt.count + (size_t)sec * Rp;
+    if (cnt[i] == 0u) return;
+    const double* mu = bt.mu + sec * bt.mu_stride();
+    double* D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    const uint32_t* arow = bt.adj + (size_t)sec * bt.C * bt.adj_copy() + (size_t)i * W;
+    for (int w = (i + 1) >> 5; w < W; ++w) {
+        uint32_t bits = arow[w];
+        while (bits) {
+            const int j = (w << 5) + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (j <= i) continue;
+            double s = 0.0;
+            for (int k = 0; k < B; ++k) s = bsmse_step(s, mu[(size_t)k * Rp + i], mu[(size_t)k * Rp + j]);
+            const double d = bsmse_finish((double)cnt[i], (double)cnt[j], s);
+            D[(size_t)i * Rp + j] = d;
+            D[(size_t)j * Rp + i] = d;
+        }
+    }
+}
+
+void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st) {
+    if (nrun == 0 || R0max == 0) return;
+    if (b.spec) {
+        const int nt = (R0max + kTile - 1) / kTile;
+        dim3 grid(nt * (nt + 1) / 2, nrun);
+        dinit_dense_kernel<<<grid, kThreads, 0, st>>>(b);
+    } else {
+        dim3 grid((R0max + kThreads - 1) / kThreads, nrun);
+        dinit_sparse_kernel<<<grid, kThreads, 0, st>>>(b);
+    }
+}
+
+// ===========================================================================
+// 2. Persistent per-section merge loop.
+// ===========================================================================
+struct Slot {
+    Pair selA, selN;   // this CTA's best adjacent / non-adjacent pair over its own rows
+    RowBest rpA, rpN;  // this CTA's partial best for row a_prev over its own columns
+};
+static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
+
+struct LoopSmem {
+    size_t slot, rslot, pscr, rscr, misc, rpart, mua, bAd, bNd, bAj, bNj, inv, cnt, total;
+};
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B) {
+    const size_t Rs = (size_t)((Rp + C - 1) / C);
+    LoopSmem L;
+    size_t o = 0;
+    L.slot = o;  o += 2 * sizeof(Slot);
+    L.rslot = o; o += kMaxCluster * sizeof(Slot);
+    L.pscr = o;  o += kWarps * sizeof(Pair);
+    L.rscr = o;  o += kWarps * sizeof(RowBest);
+    L.misc = o;  o += 64;
+    L.rpart = o; o += 2 * sizeof(RowBest);
+    L.mua = o;   o = align16(o + (size_t)B * 8);
+    L.bAd = o;   o = align16(o + Rs * 8);
+    L.bNd = o;   o = align16(o + Rs * 8);
+    L.bAj = o;   o = align16(o + Rs * 4);
+    L.bNj = o;   o = align16(o + Rs * 4);
+    L.inv = o;   o = align16(o + Rs * 4);
+    L.cnt = o;   o = align16(o + (size_t)Rp * 4);
+    L.total = o;
+    return L;
+}
+size_t hseg_loop_smem(int Rp, int C, int B) { return loop_smem_layout(Rp, C, B).total; }
+
+__device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j) {
+    if (d < kInf && (d < cd || (d == cd && j < cj))) { cd = d; cj = j; }
+}
+
+// Row-a pass over NQ columns per thread: d(a, j) for own columns j, D row/column
+// update, offer (d, a) to row j's caches, mark rows whose cached partner died.
+template <int NQ, bool SPEC>
+__device__ __forceinline__ void rowa_group(int jbase, int lo, int hi, int a, int b, double nn,
+                                           const double* __restrict__ mu, int Rp, int B,
+                                           const double* mua, const uint32_t* cnt,
+                                           const uint32_t* ra, double* __restrict__ D,
+                                           double* bAd, int* bAj, double* bNd, int* bNj,
+                                           RowBest& pA, RowBest& pN, int* inv, int* ninv) {
+    int j[NQ];
+    bool valid[NQ], isadj[NQ], need[NQ];
+    double s[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        j[q] = jbase + q * kThreads;
+        valid[q] = j[q] < hi && j[q] != a && j[q] != b && cnt[j[q]] != 0u;
+        isadj[q] = valid[q] && ((ra[j[q] >> 5] >> (j[q] & 31)) & 1u);
+        need[q] = valid[q] && (SPEC || isadj[q]);
+        s[q] = 0.0;
+    }
+#pragma unroll 4
+    for (int k = 0; k < B; ++k) {
+        const double m = mua[k];
+        const double* row = mu + (size_t)k * Rp;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (need[q]) s[q] = bsmse_step(s[q], m, row[j[q]]);
+    }
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (!valid[q]) continue;
+        const int jq = j[q];
+        double d = kInf;
+        if (need[q]) {
+            d = bsmse_finish(nn, (double)cnt[jq], s[q]);
+            D[(size_t)jq * Rp + a] = d;
+            D[(size_t)a * Rp + jq] = d;
+            if (isadj[q]) rb_offer(pA, d, jq);
+            else rb_offer(pN, d, jq);
+        }
+        const int r = jq - lo;
+        int mask = 0;
+        const int ja = bAj[r];
+        if (ja == a || ja == b) mask |= 1;
+        else if (isadj[q]) cache_offer(bAd[r], bAj[r], d, a);
+        if (SPEC) {
+            const int jn = bNj[r];
+            if (jn == a || jn == b) mask |= 2;
+            else if (!isadj[q]) cache_offer(bNd[r], bNj[r], d, a);
+        }
+        if (mask) inv[atomicAdd(ninv, 1)] = (jq << 2) | mask;
+    }
+}
+
+template <bool CLUSTER, bool SPEC>
+__global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int C = CLUSTER ? bt.C : 1;
+    const int rank = CLUSTER ? (int)cluster_rank() : 0;
+    const int sec = bt.sec0 + (int)(blockIdx.x / C);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int R0 = bt.R0[sec];
+    const int B = bt.B, Rp = bt.Rp, W = bt.W;
+    const int target = bt.target[sec];
+    const int Rs = (R0 + C - 1) / C;
+    const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
+
+    const LoopSmem L = loop_smem_layout(Rp, C, B);
+    Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
+    Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
+    Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
+    RowBest* rscr = reinterpret_cast<RowBest*>(smem + L.rscr);
+    int* misc = reinterpret_cast<int*>(smem + L.misc);
+    int& ninv = misc[0];
+    int& sdE = misc[1];
+    unsigned long long& sE0 = *reinterpret_cast<unsigned long long*>(misc + 2);
+    RowBest* rpart = reinterpret_cast<RowBest*>(smem + L.rpart);
+    double* mua = reinterpret_cast<double*>(smem + L.mua);
+    double* bAd = reinterpret_cast<double*>(smem + L.bAd);
+    double* bNd = reinterpret_cast<double*>(smem + L.bNd);
+    int* bAj = reinterpret_cast<int*>(smem + L.bAj);
+    int* bNj = reinterpret_cast<int*>(smem + L.bNj);
+    int* inv = reinterpret_cast<int*>(smem + L.inv);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
+
+    double* __restrict__ mu = bt.mu + sec * bt.mu_stride();
+    double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
+    uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * bt.adj_copy();
+
+    // Warp-cooperative rescan of one owned row from D (mask bit0: adjacent stage,
+    // bit1: non-adjacent stage) -- the full-row search of _kernels.py restricted to
+    // rows whose cached partner was merged away.
+    auto rescan = [&](int i, int mask) {
+        RowBest ba = rb_none(), bn = rb_none();
+        if (cnt[i] != 0u) {
+            const uint32_t* arow = adj + (size_t)i * W;
+            const double* drow = D + (size_t)i * Rp;
+            for (int j0 = 0; j0 < R0; j0 += 32) {
+                const int j = j0 + lane;
+                const uint32_t word = arow[j0 >> 5];
+                if (j < R0 && j != i && cnt[j] != 0u) {
+                    if ((word >> lane) & 1u) {
+                        if (mask & 1) rb_offer(ba, __ldcg(drow + j), j);
+                    } else if (SPEC && (mask & 2)) {
+                        rb_offer(bn, __ldcg(drow + j), j);
+                    }
+                }
+            }
+        }
+        ba = warp_min_rb(ba);
+        if (SPEC) bn = warp_min_rb(bn);
+        if (lane == 0) {
+            const int r = i - lo;
+            if (mask & 1) { bAd[r] = ba.d; bAj[r] = ba.j == kNoJ ? -1 : ba.j; }
+            if (SPEC && (mask & 2)) { bNd[r] = bn.d; bNj[r] = bn.j == kNoJ ? -1 : bn.j; }
+        }
+    };
+
+    // ---- prologue: counts, per-row caches, initial adjacent-pair count ----
+    for (int i = tid; i < Rp; i += kThreads) cnt[i] = i < R0 ? bt.count[(size_t)sec * Rp + i] : 0u;
+    if (tid == 0) {
+        ninv = 0;
+        sdE = 0;
+        sE0 = 0ull;
+        rpart[0] = rb_none();
+        rpart[1] = rb_none();
+    }
+    __syncthreads();
+    for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1);
+    long long E = 0;
+    if (SPEC && rank == 0) {
+        unsigned long long e = 0;
+        for (size_t w = tid; w < (size_t)R0 * W; w += kThreads) e += __popc(adj[w]);
+        atomicAdd(&sE0, e);
+    }
+    __syncthreads();
+    if (SPEC) E = (long long)(sE0 / 2);
+
+    int a_prev = -1, step = 0, conv = 0;
+    long long pairs = 0;
+    while (R0 - step > target) {
+        const int par = step & 1;
+        // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
+        Pair ca = pair_none(), cn = pair_none();
+        for (int i = lo + tid; i < hi; i += kThreads) {
+            if (cnt[i] == 0u || i == a_prev) continue;
+            const int r = i - lo;
+            if (bAj[r] >= 0) pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
+            if (SPEC && bNj[r] >= 0) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
+        }
+        if (tid == 0) ninv = 0;
+        ca = block_min_pair(ca, pscr);
+        if (SPEC) cn = block_min_pair(cn, pscr);
+        if (tid == 0) {
+            slot[par].selA = ca;
+            slot[par].selN = cn;
+            slot[par].rpA = rpart[0];
+            slot[par].rpN = rpart[1];
+        }
+        if (CLUSTER) cluster_barrier();
+        else __syncthreads();
+
+        // (B) combine the C slots: identical decision in every CTA
+        if (CLUSTER) {
+            if (tid < C * 16) {
+                const int r = tid >> 4, w = tid & 15;
+                reinterpret_cast<uint32_t*>(&rslot[r])[w] =
+                    dsmem_ld_u32(dsmem_addr(&slot[par], (unsigned)r) + 4u * w);
+            }
+            __syncthreads();
+        }
+        Pair A = pair_none(), N = pair_none();
+        RowBest PA = rb_none(), PN = rb_none();
+        for (int r = 0; r < C; ++r) {
+            const Slot& s = CLUSTER ? rslot[r] : slot[par];
+            pair_offer(A, s.selA);
+            rb_offer(PA, s.rpA.d, s.rpA.j);
+            if (SPEC) {
+                pair_offer(N, s.selN);
+                rb_offer(PN, s.rpN.d, s.rpN.j);
+            }
+        }
+        if (a_prev >= 0) {
+            if (PA.j != kNoJ) pair_offer(A, make_pair(PA.d, a_prev, PA.j));
+            if (SPEC && PN.j != kNoJ) pair_offer(N, make_pair(PN.d, a_prev, PN.j));
+            if (tid == 0 && a_prev >= lo && a_prev < hi) {
+                const int r = a_prev - lo;
+                bAd[r] = PA.d;
+                bAj[r] = PA.j == kNoJ ? -1 : PA.j;
+                if (SPEC) { bNd[r] = PN.d; bNj[r] = PN.j == kNoJ ? -1 : PN.j; }
+            }
+        }
+        // merge rule (engine.py:322-339): spectral wins iff d_s < w * d_a, strictly
+        int a = -1, b = -1, kind = 0;
+        double dch = 0.0;
+        const bool hasA = A.hi != kNoJ;
+        if (SPEC && N.hi != kNoJ) {
+            const double da = hasA ? A.d : kInf;
+            if (N.d < __dmul_rn(bt.weight, da)) { a = N.lo; b = N.hi; dch = N.d; kind = 1; }
+        }
+        if (a < 0 && hasA) { a = A.lo; b = A.hi; dch = A.d; kind = 0; }
+        if (a < 0) { conv = 1; break; }
+
+        // (C) merge (graph.py:229-264) on this CTA's private copies
+        const double nn = __dadd_rn((double)cnt[a], (double)cnt[b]);
+        const bool own_a = a >= lo && a < hi;
+        {
+            double* sa = sums + (size_t)a * B;
+            const double* sb = sums + (size_t)b * B;
+            for (int k = tid; k < B; k += kThreads) {
+                const double s = __dadd_rn(sa[k], sb[k]);
+                sa[k] = s;
+                const double m = __ddiv_rn(s, nn);
+                mua[k] = m;
+                if (own_a) mu[(size_t)k * Rp + a] = m;
+            }
+        }
+        uint32_t* ra = adj + (size_t)a * W;
+        {
+            uint32_t* rbw = adj + (size_t)b * W;
+            const int wa = a >> 5, wb = b >> 5;
+            const uint32_t ma = 1u << (a & 31), mb = 1u << (b & 31);
+            int dE = 0;
+            for (int w = tid; w < W; w += kThreads) {
+                const uint32_t oa = ra[w], ob = rbw[w];
+                uint32_t nw = oa | ob;
+                if (w == wa) nw &= ~ma;
+                if (w == wb) nw &= ~mb;
+                if (SPEC) {
+                    dE += __popc(nw) - __popc(oa) - __popc(ob);
+                    if (w == wb && (oa & mb)) dE += 1;
+                }
+                ra[w] = nw;
+                rbw[w] = 0u;
+                uint32_t bits = ob;
+                while (bits) {
+                    const int n = (w << 5) + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (n == a) continue;
+                    uint32_t* rn = adj + (size_t)n * W;
+                    if (wa == wb) rn[wa] = (rn[wa] | ma) & ~mb;
+                    else { rn[wa] |= ma; rn[wb] &= ~mb; }
+                }
+            }
+            if (SPEC && dE) atomicAdd(&sdE, dE);
+        }
+        if (tid == 0) {
+            if (own_a) {
+                bAd[a - lo] = kInf; bAj[a - lo] = -1;
+                bNd[a - lo] = kInf; bNj[a - lo] = -1;
+            }
+            if (rank == 0) {
+                const size_t o = (size_t)sec * Rp + step;
+                bt.log_a[o] = a;
+                bt.log_b[o] = b;
+                bt.log_d[o] = dch;
+                bt.log_k[o] = (uint8_t)kind;
+                bt.parent[(size_t)sec * Rp + b] = a;
+                if (SPEC) {
+                    const long long R = R0 - step;
+                    pairs += R * (R - 1) / 2 - E;
+                }
+            }
+        }
+        __syncthreads();
+        if (SPEC) E += sdE;
+
+        // (D) row-a pass over own columns (rows): fresh d(a, j), D update, cache offers
+        RowBest pA = rb_none(), pN = rb_none();
+        {
+            const int ncols = hi - lo;
+            if (ncols > 2 * kThreads) {
+                for (int jb = lo + tid; jb < hi; jb += 4 * kThreads)
+                    rowa_group<4, SPEC>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
+                                        bNd, bNj, pA, pN, inv, &ninv);
+            } else if (ncols > kThreads) {
+                rowa_group<2, SPEC>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
+                                    bNd, bNj, pA, pN, inv, &ninv);
+            } else {
+                rowa_group<1, SPEC>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
+                                    bNd, bNj, pA, pN, inv, &ninv);
+            }
+        }
+        pA = block_min_rb(pA, rscr);
+        if (SPEC) pN = block_min_rb(pN, rscr);
+        if (tid == 0) {
+            rpart[0] = pA;
+            rpart[1] = pN;
+            if (SPEC) sdE = 0;
+            cnt[a] = (uint32_t)nn;
+            cnt[b] = 0u;
+        }
+        __syncthreads();
+
+        // (E) rescan rows whose cached partner was a or b
+        const int ni = ninv;
+        for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3);
+        __syncthreads();
+        a_prev = a;
+        ++step;
+    }
+    if (CLUSTER) cluster_barrier();  // keep our slots alive until every peer is done reading
+    if (rank == 0) {
+        for (int i = tid; i < Rp; i += kThreads) bt.count[(size_t)sec * Rp + i] = cnt[i];
+        if (tid == 0) {
+            bt.nlog[sec] = step;
+            bt.conv[sec] = conv;
+            if (bt.pairs) bt.pairs[sec] = pairs;
+        }
+    }
+}
+
+int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
+    if (nrun == 0) return 0;
+    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B);
+    void (*kern)(SectionBatch);
+    if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true> : hseg_loop_kernel<true, false>;
+    else kern = b.spec ? hseg_loop_kernel<false, true> : hseg_loop_kernel<false, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (b.C > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nrun * b.C), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (b.C > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)b.C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, b);
+}
+
+}  // namespace rhseg

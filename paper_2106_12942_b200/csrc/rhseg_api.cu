@@ -1,0 +1,843 @@
+// rhseg_api.cu -- host orchestration behind the C ABI (include/rhseg_b200.h).
+//
+// Drives the quadtree exactly like SequentialExecutor.execute (recursive.py:173-209):
+// leaves (level L, row-major) -> stitch + HSEG per level L-1..1 -> assemble. Every
+// level is ONE batch: all of its sections run concurrently on the device (one
+// thread-block cluster per section, persistent merge loop), so the host only
+// launches ~5 kernels per level and synchronises once per level to size the
+// parent level (its region counts depend on how far the children merged).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rhseg_b200.h"
+#include "rhseg_batch.h"
+#include "rhseg_device.cuh"
+
+namespace rhseg {
+void launch_scan_prep(int n, int nb, int ld, int W, const double* counts, const double* sums,
+                      const int64_t* indptr, const int64_t* indices, double* mu, uint32_t* bits,
+                      bool need_bits, cudaStream_t st);
+void launch_scan_adjacent(int row_start, int row_stop, int ld, int nb, const double* counts, const double* mu,
+                          const int64_t* indptr, const int64_t* indices, double* out_d, int64_t* out_j,
+                          cudaStream_t st);
+int scan_nonadj_splits(int n, int rows, int nsm);
+void launch_scan_nonadjacent(int row_start, int row_stop, int n, int ld, int nb, int W, int nsplit,
+                             const double* counts, const double* mu, const uint32_t* bits, void* part,
+                             double* out_d, int64_t* out_j, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// small device helpers owned by the host layer
+// ---------------------------------------------------------------------------
+__global__ void compact_log_kernel(const int* la, const int* lb, const double* ld, const uint8_t* lk,
+                                   const int* nlog, const long long* off, int Rp, int* oa, int* ob,
+                                   double* od, uint8_t* ok) {
+    const int s = blockIdx.x;
+    const int n = nlog[s];
+    const long long o = off[s];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const size_t src = (size_t)s * Rp + k;
+        oa[o + k] = la[src];
+        ob[o + k] = lb[src];
+        od[o + k] = ld[src];
+        ok[o + k] = lk[src];
+    }
+}
+
+__global__ void fp64_probe_kernel(double* out, int iters) {
+    double x[8], y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        x[q] = 1.0 + 1e-3 * (threadIdx.x + q);
+        y[q] = 0.0;
+    }
+    const double m = 1.0000001;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = bsmse_step(y[q], x[q], m);  // sub, mul, add
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += y[q];
+    if (s == 12345.0) out[threadIdx.x] = s;  // keep the loop alive
+}
+
+}  // namespace rhseg
+
+using namespace rhseg;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+#define CK(expr)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(RHSEG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+    } while (0)
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---------------------------------------------------------------------------
+// one batch of sections (a quadtree level or a standalone graph)
+// ---------------------------------------------------------------------------
+struct Level {
+    int level = 0, side = 0, nsec = 0, edge = 0, Rp = 0, W = 0, C = 1, B = 0, R0max = 0;
+    std::vector<int> R0h, tgth, nlogh, convh;
+    std::vector<long long> pairsh;
+    SectionBatch sb{};
+    void* keep = nullptr;
+    void* work = nullptr;
+    int* map = nullptr;    // dense-renumber scratch used when this level is stitched
+    size_t work_zero = 0;  // bytes at the start of `work` that must be zeroed (adjacency)
+    bool done = false;
+};
+
+struct rhseg_ctx {
+    int device = 0;
+    int nsm = 148;
+    cudaStream_t stream = nullptr;
+    std::vector<Level> levels;  // processing order == log order (L .. 1)
+    bool have = false;
+    int edge = 0, bands = 0, L = 0;
+    // root snapshots (copy 0 of the private per-CTA state)
+    void* snap = nullptr;
+    uint32_t* init_count = nullptr;
+    double* init_sums = nullptr;
+    uint32_t* init_adj = nullptr;
+    int* init_assign = nullptr;
+    int root_initial_live = 0;
+    int* labels = nullptr;  // [edge*edge]
+    int* lab_first = nullptr;
+    int* lab_rank = nullptr;
+    void* dmat = nullptr;
+    size_t dmat_bytes = 0;
+    rhseg_result_info info{};
+    float phase_ms[4] = {0, 0, 0, 0};
+    bool phases_valid = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+};
+
+static cudaEvent_t ev_get(rhseg_ctx* c) {
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+struct PhaseTimer {
+    rhseg_ctx* c;
+    int phase;
+    cudaStream_t st;
+    cudaEvent_t a;
+    PhaseTimer(rhseg_ctx* c_, int p, cudaStream_t s) : c(c_), phase(p), st(s) {
+        a = ev_get(c);
+        cudaEventRecord(a, st);
+    }
+    ~PhaseTimer() {
+        cudaEvent_t b = ev_get(c);
+        cudaEventRecord(b, st);
+        c->evs.push_back({phase, {a, b}});
+    }
+};
+
+static void free_level(Level& lv, cudaStream_t st) {
+    if (lv.work) cudaFreeAsync(lv.work, st);
+    if (lv.keep) cudaFreeAsync(lv.keep, st);
+    lv.work = lv.keep = nullptr;
+}
+static void free_work(Level& lv, cudaStream_t st) {
+    if (lv.work) cudaFreeAsync(lv.work, st);
+    lv.work = nullptr;
+}
+
+static void reset_ctx(rhseg_ctx* c, cudaStream_t st) {
+    for (auto& lv : c->levels) free_level(lv, st);
+    c->levels.clear();
+    if (c->snap) cudaFreeAsync(c->snap, st);
+    c->snap = nullptr;
+    c->have = false;
+    c->phases_valid = false;
+    c->evs.clear();
+    c->ev_used = 0;
+    memset(&c->info, 0, sizeof(c->info));
+}
+
+static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced) {
+    if (forced > 0) return forced;
+    if (R0max < 512) return 1;
+    int C = 1;
+    while (C * 2 <= kMaxCluster && nsec * C * 2 <= c->nsm && R0max / (C * 2) >= 128) C *= 2;
+    return C;
+}
+
+// Allocate and zero one level's device state. R0h/tgth must be filled.
+static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, int forced_C) {
+    lv.R0max = 0;
+    for (int r : lv.R0h) lv.R0max = std::max(lv.R0max, r);
+    if (lv.R0max > 16384)
+        return fail(RHSEG_E_TOO_LARGE, "section with " + std::to_string(lv.R0max) + " regions exceeds 16384");
+    lv.Rp = std::max(64, (lv.R0max + 63) / 64 * 64);
+    lv.W = lv.Rp / 32;
+    lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
+    if (hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024) {
+        // grow the cluster until the per-CTA row slice fits shared memory
+        while (lv.C < kMaxCluster && hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024) lv.C *= 2;
+        if (hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024)
+            return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
+    }
+    const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
+                 C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
+    // keep block
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align256(o + bytes);
+        return at;
+    };
+    const size_t oR0 = take(ns * 4), oT = take(ns * 4), oCnt = take(ns * Rp * 4), oPar = take(ns * Rp * 4),
+                 oAs = take(ns * npx * 4), oMap = take(ns * Rp * 4), oLa = take(ns * Rp * 4),
+                 oLb = take(ns * Rp * 4), oLd = take(ns * Rp * 8), oLk = take(ns * Rp), oN = take(ns * 4),
+                 oCv = take(ns * 4), oPr = take(ns * 8);
+    const size_t keep_bytes = o;
+    CK(cudaMallocAsync(&lv.keep, keep_bytes, st));
+    CK(cudaMemsetAsync(lv.keep, 0, keep_bytes, st));
+    o = 0;
+    const size_t oAdj = take(ns * C * Rp * W * 4);
+    lv.work_zero = o;
+    const size_t oMu = take(ns * B * Rp * 8), oSums = take(ns * C * Rp * B * 8);
+    const size_t work_bytes = o;
+    CK(cudaMallocAsync(&lv.work, work_bytes, st));
+    CK(cudaMemsetAsync(lv.work, 0, lv.work_zero, st));
+    char* K = static_cast<char*>(lv.keep);
+    char* Wk = static_cast<char*>(lv.work);
+    SectionBatch& b = lv.sb;
+    b = SectionBatch{};
+    b.nsec = lv.nsec;
+    b.B = lv.B;
+    b.Rp = lv.Rp;
+    b.W = lv.W;
+    b.C = lv.C;
+    b.edge = lv.edge;
+    b.npx = (int)npx;
+    b.spec = weight > 0.0 ? 1 : 0;
+    b.weight = weight;
+    b.R0 = reinterpret_cast<int*>(K + oR0);
+    b.target = reinterpret_cast<int*>(K + oT);
+    b.count = reinterpret_cast<uint32_t*>(K + oCnt);
+    b.parent = reinterpret_cast<int*>(K + oPar);
+    b.assign = reinterpret_cast<int*>(K + oAs);
+    b.log_a = reinterpret_cast<int*>(K + oLa);
+    b.log_b = reinterpret_cast<int*>(K + oLb);
+    b.log_d = reinterpret_cast<double*>(K + oLd);
+    b.log_k = reinterpret_cast<uint8_t*>(K + oLk);
+    b.nlog = reinterpret_cast<int*>(K + oN);
+    b.conv = reinterpret_cast<int*>(K + oCv);
+    b.pairs = reinterpret_cast<long long*>(K + oPr);
+    b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
+    b.mu = reinterpret_cast<double*>(Wk + oMu);
+    b.sums = reinterpret_cast<double*>(Wk + oSums);
+    lv.map = reinterpret_cast<int*>(K + oMap);
+    CK(cudaMemcpyAsync(const_cast<int*>(b.R0), lv.R0h.data(), ns * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(const_cast<int*>(b.target), lv.tgth.data(), ns * 4, cudaMemcpyHostToDevice, st));
+    return RHSEG_OK;
+}
+// dinit + merge loop over D-sized chunks of sections, then union-find resolve.
+static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
+    const size_t dsec = (size_t)lv.Rp * lv.Rp * 8;
+    size_t freeb = 0, totalb = 0;
+    CK(cudaMemGetInfo(&freeb, &totalb));
+    size_t budget = (size_t)(0.6 * (double)(freeb + c->dmat_bytes));
+    size_t chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, budget / dsec));
+    if (c->dmat_bytes < chunk * dsec) {
+        if (c->dmat) CK(cudaFreeAsync(c->dmat, st));
+        c->dmat = nullptr;
+        c->dmat_bytes = 0;
+        CK(cudaMallocAsync(&c->dmat, chunk * dsec, st));
+        c->dmat_bytes = chunk * dsec;
+    }
+    lv.sb.D = static_cast<double*>(c->dmat);
+    for (size_t s0 = 0; s0 < (size_t)lv.nsec; s0 += chunk) {
+        const int n = (int)std::min(chunk, (size_t)lv.nsec - s0);
+        SectionBatch b = lv.sb;
+        b.sec0 = (int)s0;
+        {
+            PhaseTimer t(c, 1, st);
+            launch_dinit(b, n, lv.R0max, st);
+        }
+        CK(cudaGetLastError());
+        {
+            PhaseTimer t(c, 2, st);
+            int e = launch_hseg_loop(b, n, st);
+            if (e != cudaSuccess)
+                return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
+        }
+        CK(cudaGetLastError());
+    }
+    {
+        PhaseTimer t(c, 3, st);
+        launch_resolve(lv.sb, st);
+    }
+    CK(cudaGetLastError());
+    lv.nlogh.resize(lv.nsec);
+    lv.convh.resize(lv.nsec);
+    lv.pairsh.resize(lv.nsec);
+    CK(cudaMemcpyAsync(lv.nlogh.data(), lv.sb.nlog, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lv.convh.data(), lv.sb.conv, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lv.pairsh.data(), lv.sb.pairs, 8 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    lv.done = true;
+    return RHSEG_OK;
+}
+
+static int snapshot_root(rhseg_ctx* c, Level& lv, cudaStream_t st) {
+    const size_t Rp = lv.Rp, B = lv.B, W = lv.W, npx = (size_t)lv.edge * lv.edge;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align256(o + bytes);
+        return at;
+    };
+    const size_t oc = take(Rp * 4), os = take(Rp * B * 8), oa = take(Rp * W * 4), oas = take(npx * 4),
+                 olab = take(npx * 4), of = take(Rp * 4), orank = take(Rp * 4);
+    CK(cudaMallocAsync(&c->snap, o, st));
+    char* S = static_cast<char*>(c->snap);
+    c->init_count = reinterpret_cast<uint32_t*>(S + oc);
+    c->init_sums = reinterpret_cast<double*>(S + os);
+    c->init_adj = reinterpret_cast<uint32_t*>(S + oa);
+    c->init_assign = reinterpret_cast<int*>(S + oas);
+    c->labels = reinterpret_cast<int*>(S + olab);
+    c->lab_first = reinterpret_cast<int*>(S + of);
+    c->lab_rank = reinterpret_cast<int*>(S + orank);
+    CK(cudaMemcpyAsync(c->init_count, lv.sb.count, Rp * 4, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->init_sums, lv.sb.sums, Rp * B * 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(c->init_adj, lv.sb.adj, Rp * W * 4, cudaMemcpyDeviceToDevice, st));
+    if (npx) CK(cudaMemcpyAsync(c->init_assign, lv.sb.assign, npx * 4, cudaMemcpyDeviceToDevice, st));
+    c->root_initial_live = lv.R0h[0];
+    return RHSEG_OK;
+}
+
+static void finish_info(rhseg_ctx* c) {
+    rhseg_result_info& I = c->info;
+    I.n_records = 0;
+    I.spectral_pairs = 0;
+    I.n_sections = 0;
+    I.converged_early = 0;
+    for (auto& lv : c->levels) {
+        for (int s = 0; s < lv.nsec; ++s) {
+            I.n_records += lv.nlogh[s];
+            I.spectral_pairs += lv.pairsh[s];
+            I.converged_early |= lv.convh[s] ? 1 : 0;
+        }
+        I.n_sections += lv.nsec;
+    }
+    Level& root = c->levels.back();
+    I.levels = c->L;
+    I.edge = c->edge;
+    I.bands = c->bands;
+    I.root_idspace = root.R0h[0];
+    I.root_initial_regions = c->root_initial_live;
+    I.root_regions = root.R0h[0] - root.nlogh[0];
+}
+
+static void finish_phases(rhseg_ctx* c) {
+    for (int p = 0; p < 4; ++p) c->phase_ms[p] = 0.f;
+    for (auto& e : c->evs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e.second.first, e.second.second);
+        c->phase_ms[e.first] += ms;
+    }
+    c->phases_valid = true;
+}
+
+static int validate(const rhseg_params* p, int edge, int bands) {
+    if (!p) return fail(RHSEG_E_INVALID, "params is NULL");
+    if (!(p->spectral_weight >= 0.0 && p->spectral_weight <= 1.0))
+        return fail(RHSEG_E_INVALID, "spectral_weight must be in [0, 1]");
+    if (p->target_regions < 1) return fail(RHSEG_E_INVALID, "target_regions must be >= 1");
+    if (p->section_target_regions < 0) return fail(RHSEG_E_INVALID, "section_target_regions must be >= 1");
+    if (p->levels < 1) return fail(RHSEG_E_INVALID, "levels must be >= 1");
+    if (p->connectivity != 4 && p->connectivity != 8) return fail(RHSEG_E_INVALID, "connectivity must be 4 or 8");
+    if (p->measure != 0) return fail(RHSEG_E_INVALID, "unknown measure; available: ['sqrt-bsmse']");
+    if (edge < 1 || bands < 1) return fail(RHSEG_E_INVALID, "width and bands must be >= 1");
+    if (p->levels > 30) return fail(RHSEG_E_INVALID, "levels too large");
+    const long long side = 1LL << (p->levels - 1);
+    if (edge % side != 0)
+        return fail(RHSEG_E_INDIVISIBLE, "edge " + std::to_string(edge) + " not divisible by " +
+                                             std::to_string(side) + " (levels=" + std::to_string(p->levels) + ")");
+    if (p->cluster != 0 && p->cluster != 1 && p->cluster != 2 && p->cluster != 4 && p->cluster != 8 &&
+        p->cluster != 16)
+        return fail(RHSEG_E_INVALID, "cluster must be 0 (auto) or one of 1,2,4,8,16");
+    return RHSEG_OK;
+}
+
+static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int bands, const rhseg_params* p,
+                           cudaStream_t st) {
+    int rc = validate(p, edge, bands);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    reset_ctx(c, st);
+    c->edge = edge;
+    c->bands = bands;
+    c->L = p->levels;
+    const int L = p->levels;
+    const int sect = p->section_target_regions > 0 ? p->section_target_regions : p->target_regions;
+    const int side = 1 << (L - 1);
+    const int e = edge / side;
+    if ((long long)e * e > 16384) return fail(RHSEG_E_TOO_LARGE, "leaf sections above 128x128 pixels are not supported");
+    c->levels.reserve(L);
+    // ---- leaves ----
+    {
+        c->levels.emplace_back();
+        Level& lv = c->levels.back();
+        lv.level = L;
+        lv.side = side;
+        lv.nsec = side * side;
+        lv.edge = e;
+        lv.B = bands;
+        lv.R0h.assign(lv.nsec, e * e);
+        lv.tgth.assign(lv.nsec, L == 1 ? p->target_regions : sect);
+        rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster);
+        if (rc) return rc;
+        {
+            PhaseTimer t(c, 0, st);
+            launch_leaf_init(lv.sb, d_samples, edge, side, p->connectivity, st);
+        }
+        CK(cudaGetLastError());
+        if (L == 1) {
+            rc = snapshot_root(c, lv, st);
+            if (rc) return rc;
+        }
+        rc = run_level(c, lv, st);
+        if (rc) return rc;
+    }
+    // ---- upper levels ----
+    for (int level = L - 1; level >= 1; --level) {
+        Level& ch = c->levels.back();
+        Level pa;
+        pa.level = level;
+        pa.side = 1 << (level - 1);
+        pa.nsec = pa.side * pa.side;
+        pa.edge = ch.edge * 2;
+        pa.B = bands;
+        pa.R0h.assign(pa.nsec, 0);
+        for (int P = 0; P < pa.nsec; ++P) {
+            const int pr = P / pa.side, pc = P % pa.side;
+            for (int k = 0; k < 4; ++k) {
+                const int ci = (2 * pr + (k >> 1)) * ch.side + (2 * pc + (k & 1));
+                pa.R0h[P] += ch.R0h[ci] - ch.nlogh[ci];
+            }
+        }
+        pa.tgth.assign(pa.nsec, level == 1 ? p->target_regions : sect);
+        rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster);
+        if (rc) return rc;
+        {
+            PhaseTimer t(c, 0, st);
+            launch_stitch(ch.sb, ch.side, pa.sb, pa.side, nullptr, ch.map, p->connectivity, st);
+        }
+        CK(cudaGetLastError());
+        free_work(ch, st);
+        c->levels.push_back(std::move(pa));
+        Level& lv = c->levels.back();
+        if (level == 1) {
+            rc = snapshot_root(c, lv, st);
+            if (rc) return rc;
+        }
+        rc = run_level(c, lv, st);
+        if (rc) return rc;
+    }
+    // ---- dense labels of the root ----
+    Level& root = c->levels.back();
+    {
+        PhaseTimer t(c, 3, st);
+        launch_dense_labels(root.sb.assign, edge * edge, root.Rp, c->lab_first, c->lab_rank, c->labels, st);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    c->have = true;
+    finish_info(c);
+    finish_phases(c);
+    return RHSEG_OK;
+}
+
+// ===========================================================================
+// exported C ABI
+// ===========================================================================
+extern "C" {
+
+int rhseg_abi_version(void) { return RHSEG_ABI_VERSION; }
+const char* rhseg_last_error(void) { return g_err.c_str(); }
+
+int rhseg_ctx_create(int device, rhseg_ctx** out) {
+    if (!out) return fail(RHSEG_E_INVALID, "out is NULL");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(RHSEG_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(RHSEG_E_INVALID, "bad device index");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(RHSEG_E_CUDA, std::string("librhseg_b200 is built for sm_100a; device is ") + prop.name);
+    rhseg_ctx* c = new rhseg_ctx();
+    c->device = device;
+    c->nsm = prop.multiProcessorCount;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+    return RHSEG_OK;
+}
+
+int rhseg_ctx_destroy(rhseg_ctx* c) {
+    if (!c) return RHSEG_OK;
+    cudaSetDevice(c->device);
+    reset_ctx(c, c->stream);
+    if (c->dmat) cudaFreeAsync(c->dmat, c->stream);
+    cudaStreamSynchronize(c->stream);
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return RHSEG_OK;
+}
+
+int rhseg_run_device(rhseg_ctx* c, const float* d_samples, int32_t edge, int32_t bands, const rhseg_params* p,
+                     void* stream) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    return run_device_impl(c, d_samples, edge, bands, p, st);
+}
+
+int rhseg_result_info_get(rhseg_ctx* c, rhseg_result_info* info) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    *info = c->info;
+    info->device_ms = c->phase_ms[0] + c->phase_ms[1] + c->phase_ms[2] + c->phase_ms[3];
+    return RHSEG_OK;
+}
+
+int rhseg_result_phase_ms(rhseg_ctx* c, float* ms4) {
+    if (!c || !c->phases_valid) return fail(RHSEG_E_STATE, "no timed run");
+    for (int p = 0; p < 4; ++p) ms4[p] = c->phase_ms[p];
+    return RHSEG_OK;
+}
+
+int rhseg_result_sections(rhseg_ctx* c, int32_t* level, int32_t* row, int32_t* col, int64_t* offset,
+                          int64_t* count) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    int64_t off = 0;
+    int k = 0;
+    for (auto& lv : c->levels)
+        for (int s = 0; s < lv.nsec; ++s, ++k) {
+            if (level) level[k] = lv.level;
+            if (row) row[k] = s / lv.side;
+            if (col) col[k] = s % lv.side;
+            if (offset) offset[k] = off;
+            if (count) count[k] = lv.nlogh[s];
+            off += lv.nlogh[s];
+        }
+    return RHSEG_OK;
+}
+
+static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t* sk, cudaStream_t st) {
+    const int64_t n = c->info.n_records;
+    if (n == 0) return RHSEG_OK;
+    int* da = nullptr;
+    CK(cudaMallocAsync(&da, (size_t)n * 17 + 1024, st));
+    int* db = da + n;
+    double* dd = reinterpret_cast<double*>(db + n);
+    uint8_t* dk = reinterpret_cast<uint8_t*>(dd + n);
+    int64_t base = 0;
+    std::vector<long long> off;
+    long long* doff = nullptr;
+    for (auto& lv : c->levels) {
+        off.resize(lv.nsec);
+        long long o = 0;
+        for (int s = 0; s < lv.nsec; ++s) {
+            off[s] = o;
+            o += lv.nlogh[s];
+        }
+        if (o == 0) continue;
+        CK(cudaMallocAsync(&doff, 8 * (size_t)lv.nsec, st));
+        CK(cudaMemcpyAsync(doff, off.data(), 8 * (size_t)lv.nsec, cudaMemcpyHostToDevice, st));
+        compact_log_kernel<<<lv.nsec, 256, 0, st>>>(lv.sb.log_a, lv.sb.log_b, lv.sb.log_d, lv.sb.log_k, lv.sb.nlog,
+                                                    doff, lv.Rp, da + base, db + base, dd + base, dk + base);
+        CK(cudaGetLastError());
+        CK(cudaFreeAsync(doff, st));
+        CK(cudaStreamSynchronize(st));  // `off` is reused next level
+        base += o;
+    }
+    if (sa) CK(cudaMemcpyAsync(sa, da, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (sb) CK(cudaMemcpyAsync(sb, db, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (sd) CK(cudaMemcpyAsync(sd, dd, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    if (sk) CK(cudaMemcpyAsync(sk, dk, (size_t)n, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(da, st));
+    CK(cudaStreamSynchronize(st));
+    return RHSEG_OK;
+}
+
+int rhseg_result_log(rhseg_ctx* c, int32_t* survivor, int32_t* absorbed, double* dissim, uint8_t* kind) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    CK(cudaSetDevice(c->device));
+    return copy_log(c, survivor, absorbed, dissim, kind, c->stream);
+}
+
+int rhseg_result_labels(rhseg_ctx* c, int32_t* labels, int32_t* assignment) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    CK(cudaSetDevice(c->device));
+    const size_t npx = (size_t)c->edge * c->edge;
+    if (labels) CK(cudaMemcpyAsync(labels, c->labels, npx * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (assignment)
+        CK(cudaMemcpyAsync(assignment, c->levels.back().sb.assign, npx * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return RHSEG_OK;
+}
+
+int rhseg_result_root(rhseg_ctx* c, int32_t which, int64_t* counts, double* sums, uint32_t* adjacency,
+                      int32_t* assignment) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    CK(cudaSetDevice(c->device));
+    Level& root = c->levels.back();
+    const size_t R = (size_t)root.R0h[0], B = (size_t)root.B, Rp = root.Rp, W = root.W;
+    const size_t Wo = (R + 31) / 32, npx = (size_t)c->edge * c->edge;
+    const uint32_t* cnt = which == 0 ? c->init_count : root.sb.count;
+    const double* sm = which == 0 ? c->init_sums : root.sb.sums;
+    const uint32_t* ad = which == 0 ? c->init_adj : root.sb.adj;
+    const int* as = which == 0 ? c->init_assign : root.sb.assign;
+    std::vector<uint32_t> hc(Rp);
+    CK(cudaMemcpyAsync(hc.data(), cnt, Rp * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (sums) CK(cudaMemcpyAsync(sums, sm, R * B * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (adjacency)
+        CK(cudaMemcpy2DAsync(adjacency, Wo * 4, ad, W * 4, Wo * 4, R, cudaMemcpyDeviceToHost, c->stream));
+    if (assignment) CK(cudaMemcpyAsync(assignment, as, npx * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (counts)
+        for (size_t i = 0; i < R; ++i) counts[i] = hc[i];
+    return RHSEG_OK;
+}
+
+int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t bands, const rhseg_params* p,
+                   void* stream, int32_t* log_survivor, int32_t* log_absorbed, double* log_dissim,
+                   uint8_t* log_kind, int32_t* labels, rhseg_result_info* info) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    int rc = validate(p, edge, bands);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    const size_t bytes = (size_t)edge * edge * bands * sizeof(float);
+    float* d = nullptr;
+    CK(cudaMallocAsync(&d, bytes, st));
+    CK(cudaMemcpyAsync(d, h_samples, bytes, cudaMemcpyHostToDevice, st));
+    rc = run_device_impl(c, d, edge, bands, p, st);
+    cudaFreeAsync(d, st);
+    if (rc) return rc;
+    rc = copy_log(c, log_survivor, log_absorbed, log_dissim, log_kind, st);
+    if (rc) return rc;
+    if (labels) {
+        CK(cudaMemcpyAsync(labels, c->labels, (size_t)edge * edge * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    if (info) rhseg_result_info_get(c, info);
+    return RHSEG_OK;
+}
+
+int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* counts, const double* sums,
+                     const int64_t* indptr, const int64_t* indices, double weight, int64_t target, int32_t cluster,
+                     int32_t* log_survivor, int32_t* log_absorbed, double* log_dissim, uint8_t* log_kind,
+                     int64_t* n_records, int32_t* converged_early) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    if (!(weight >= 0.0 && weight <= 1.0)) return fail(RHSEG_E_INVALID, "spectral_weight must be in [0, 1]");
+    if (target < 1) return fail(RHSEG_E_INVALID, "target_regions must be >= 1");
+    if (n < 0 || nbands < 1) return fail(RHSEG_E_INVALID, "bad graph shape");
+    if (n > 16384) return fail(RHSEG_E_TOO_LARGE, "graph exceeds 16384 regions");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    reset_ctx(c, st);
+    if (n == 0) {
+        *n_records = 0;
+        *converged_early = 0;
+        return RHSEG_OK;
+    }
+    c->levels.emplace_back();
+    Level& lv = c->levels.back();
+    lv.level = 1;
+    lv.side = 1;
+    lv.nsec = 1;
+    lv.edge = 0;
+    lv.B = (int)nbands;
+    lv.R0h.assign(1, (int)n);
+    lv.tgth.assign(1, (int)std::min<int64_t>(target, INT32_MAX));
+    int rc = alloc_level(c, lv, weight, st, cluster);
+    if (rc) return rc;
+    const int64_t nnz = indptr[n];
+    void* tmp = nullptr;
+    const size_t b_counts = align256(8 * (size_t)n), b_sums = align256(8 * (size_t)n * nbands),
+                 b_ptr = align256(8 * (size_t)(n + 1)), b_idx = align256(8 * (size_t)std::max<int64_t>(nnz, 1));
+    CK(cudaMallocAsync(&tmp, b_counts + b_sums + b_ptr + b_idx, st));
+    char* T = static_cast<char*>(tmp);
+    double* dc = reinterpret_cast<double*>(T);
+    double* ds = reinterpret_cast<double*>(T + b_counts);
+    int64_t* dp = reinterpret_cast<int64_t*>(T + b_counts + b_sums);
+    int64_t* di = reinterpret_cast<int64_t*>(T + b_counts + b_sums + b_ptr);
+    CK(cudaMemcpyAsync(dc, counts, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ds, sums, 8 * (size_t)n * nbands, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dp, indptr, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) CK(cudaMemcpyAsync(di, indices, 8 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    {
+        PhaseTimer t(c, 0, st);
+        launch_graph_init(lv.sb, dc, ds, dp, di, st);
+    }
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(tmp, st));
+    rc = run_level(c, lv, st);
+    if (rc) return rc;
+    const int nrec = lv.nlogh[0];
+    if (nrec) {
+        if (log_survivor) CK(cudaMemcpyAsync(log_survivor, lv.sb.log_a, 4 * (size_t)nrec, cudaMemcpyDeviceToHost, st));
+        if (log_absorbed) CK(cudaMemcpyAsync(log_absorbed, lv.sb.log_b, 4 * (size_t)nrec, cudaMemcpyDeviceToHost, st));
+        if (log_dissim) CK(cudaMemcpyAsync(log_dissim, lv.sb.log_d, 8 * (size_t)nrec, cudaMemcpyDeviceToHost, st));
+        if (log_kind) CK(cudaMemcpyAsync(log_kind, lv.sb.log_k, (size_t)nrec, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    *n_records = nrec;
+    *converged_early = lv.convh[0];
+    finish_phases(c);
+    return RHSEG_OK;
+}
+
+// ---- B3 ---------------------------------------------------------------------
+struct ScanState {
+    std::mutex mu;
+    bool init = false;
+    int device = 0, nsm = 148;
+    cudaStream_t st = nullptr;
+    void* buf = nullptr;
+    size_t cap = 0;
+};
+static ScanState g_scan;
+
+static int scan_common(int64_t row_start, int64_t row_stop, int64_t n, int64_t nb, const double* counts,
+                       const double* sums, const int64_t* indptr, const int64_t* indices, double* out_d,
+                       int64_t* out_j, bool nonadj) {
+    if (row_start < 0 || row_stop > n || row_start > row_stop) return fail(RHSEG_E_INVALID, "bad row range");
+    if (n > INT32_MAX / 2 || nb < 0) return fail(RHSEG_E_INVALID, "bad shape");
+    if (row_start == row_stop) return RHSEG_OK;
+    std::lock_guard<std::mutex> lock(g_scan.mu);
+    if (!g_scan.init) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(RHSEG_E_CUDA, "no CUDA device");
+        CK(cudaGetDevice(&g_scan.device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, g_scan.device));
+        if (prop.major != 10) return fail(RHSEG_E_CUDA, "librhseg_b200 is built for sm_100a");
+        g_scan.nsm = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&g_scan.st, cudaStreamNonBlocking));
+        g_scan.init = true;
+    }
+    CK(cudaSetDevice(g_scan.device));
+    cudaStream_t st = g_scan.st;
+    const int ni = (int)n, nbi = (int)nb, ld = std::max(64, (ni + 63) / 64 * 64), W = ld / 32;
+    const int64_t nnz = indptr[n];
+    const int rows = (int)(row_stop - row_start);
+    const int nsplit = nonadj ? scan_nonadj_splits(ni, rows, g_scan.nsm) : 1;
+    const size_t b_c = align256(8 * (size_t)n), b_s = align256(8 * (size_t)n * std::max<int64_t>(nb, 1)),
+                 b_p = align256(8 * (size_t)(n + 1)), b_i = align256(8 * (size_t)std::max<int64_t>(nnz, 1)),
+                 b_mu = align256(8 * (size_t)ld * std::max<int64_t>(nb, 1)),
+                 b_bits = nonadj ? align256(4 * (size_t)ni * W) : 0,
+                 b_part = nonadj ? align256(sizeof(RowBest) * (size_t)nsplit * ld) : 0, b_od = align256(8 * (size_t)n),
+                 b_oj = align256(8 * (size_t)n);
+    const size_t total = b_c + b_s + b_p + b_i + b_mu + b_bits + b_part + b_od + b_oj;
+    if (g_scan.cap < total) {
+        if (g_scan.buf) CK(cudaFree(g_scan.buf));
+        g_scan.buf = nullptr;
+        CK(cudaMalloc(&g_scan.buf, total));
+        g_scan.cap = total;
+    }
+    char* P = static_cast<char*>(g_scan.buf);
+    double* dc = reinterpret_cast<double*>(P);
+    P += b_c;
+    double* ds = reinterpret_cast<double*>(P);
+    P += b_s;
+    int64_t* dp = reinterpret_cast<int64_t*>(P);
+    P += b_p;
+    int64_t* di = reinterpret_cast<int64_t*>(P);
+    P += b_i;
+    double* dmu = reinterpret_cast<double*>(P);
+    P += b_mu;
+    uint32_t* dbits = reinterpret_cast<uint32_t*>(P);
+    P += b_bits;
+    void* dpart = P;
+    P += b_part;
+    double* dod = reinterpret_cast<double*>(P);
+    P += b_od;
+    int64_t* doj = reinterpret_cast<int64_t*>(P);
+    CK(cudaMemcpyAsync(dc, counts, 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    if (nb) CK(cudaMemcpyAsync(ds, sums, 8 * (size_t)n * nb, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dp, indptr, 8 * (size_t)(n + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) CK(cudaMemcpyAsync(di, indices, 8 * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    launch_scan_prep(ni, nbi, ld, W, dc, ds, dp, di, dmu, dbits, nonadj, st);
+    if (nonadj)
+        launch_scan_nonadjacent((int)row_start, (int)row_stop, ni, ld, nbi, W, nsplit, dc, dmu, dbits, dpart, dod, doj,
+                                st);
+    else
+        launch_scan_adjacent((int)row_start, (int)row_stop, ld, nbi, dc, dmu, dp, di, dod, doj, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out_d + row_start, dod + row_start, 8 * (size_t)rows, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_j + row_start, doj + row_start, 8 * (size_t)rows, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return RHSEG_OK;
+}
+
+int rhseg_scan_adjacent(int64_t row_start, int64_t row_stop, int64_t n, int64_t nbands, const double* counts,
+                        const double* sums, const int64_t* indptr, const int64_t* indices, double* out_d,
+                        int64_t* out_j) {
+    return scan_common(row_start, row_stop, n, nbands, counts, sums, indptr, indices, out_d, out_j, false);
+}
+
+int rhseg_scan_nonadjacent(int64_t row_start, int64_t row_stop, int64_t col_tile, int64_t n, int64_t nbands,
+                           const double* counts, const double* sums, const int64_t* indptr, const int64_t* indices,
+                           double* out_d, int64_t* out_j) {
+    (void)col_tile;  // result-invariant in the reference (_kernels.py:66-72)
+    return scan_common(row_start, row_stop, n, nbands, counts, sums, indptr, indices, out_d, out_j, true);
+}
+
+int rhseg_fp64_peak(rhseg_ctx* c, double* ops_per_s) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    CK(cudaSetDevice(c->device));
+    double* out = nullptr;
+    CK(cudaMalloc(&out, 1024 * sizeof(double)));
+    const int blocks = c->nsm * 8, threads = 256, iters = 20000;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp64_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 100);
+    cudaEventRecord(a, c->stream);
+    fp64_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, iters);
+    cudaEventRecord(b, c->stream);
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *ops_per_s = (double)blocks * threads * iters * 8.0 * 3.0 / (ms * 1e-3);
+    return RHSEG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// rhseg_batch.h -- the HBM layout of one batch of independent HSEG sections
+// (one quadtree level, or one standalone region graph). Shared by the host
+// orchestration (rhseg_api.cu) and the kernels.
+//
+// Per section s (all arrays padded to Rp = roundup(R0max, 32) region slots):
+//   count [Rp]          u32   pixel counts (0 = dead)      -- graph.py:86-92 pixel_count
+//   mu    [B][Rp]       f64   band-major mean cache        -- sums/count (Appendix A.3)
+//   D     [Rp][Rp]      f64   dissimilarity matrix, kept exact for every live pair
+//                             (w > 0) or every adjacent pair (w = 0)
+//   sums  [C][Rp][B]    f64   band sums, one private copy per cluster CTA
+//   adj   [C][Rp][W]    u32   symmetric adjacency bitset, one private copy per CTA
+//   parent[Rp]          i32   absorbed -> survivor (union-find for labels), -1 = root
+//   assign[npx]         i32   pixel -> section-local region id
+//   log_{a,b,d,k}[Rp]         merge records (survivor, absorbed, dissim, kind)
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+namespace rhseg {
+
+struct SectionBatch {
+    int nsec;      // sections in the batch
+    int B;         // bands
+    int Rp;        // padded region capacity (multiple of 32)
+    int W;         // Rp / 32 bitset words per row
+    int C;         // CTAs per section (thread-block cluster size)
+    int edge;      // section edge in pixels (0 for a standalone graph)
+    int npx;       // edge * edge
+    int spec;      // spectral stage on (weight > 0)
+    double weight; // spectral_weight (engine.py:33)
+    const int* R0;       // [nsec] initial live regions
+    const int* target;   // [nsec] stopping count (recursive.py:49-52)
+    double* mu;
+    double* D;
+    double* sums;
+    uint32_t* adj;
+    uint32_t* count;
+    int* parent;
+    int* assign;
+    int* log_a;
+    int* log_b;
+    double* log_d;
+    uint8_t* log_k;
+    int* nlog;
+    int* conv;
+    long long* pairs;    // [nsec] reference-equivalent spectral pairs, sum_steps R(R-1)/2 - E
+    int sec0;            // first section covered by D (D is allocated per launch chunk)
+
+    __host__ __device__ size_t mu_stride() const { return (size_t)B * Rp; }
+    __host__ __device__ size_t d_stride() const { return (size_t)Rp * Rp; }
+    __host__ __device__ size_t sums_copy() const { return (size_t)Rp * B; }
+    __host__ __device__ size_t adj_copy() const { return (size_t)Rp * W; }
+};
+
+// Kernel launchers (hseg_kernels.cu / section_kernels.cu). All stream-ordered.
+void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
+int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
+size_t hseg_loop_smem(int Rp, int C, int B);
+void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int side,
+                      int connectivity, cudaStream_t st);
+void launch_resolve(const SectionBatch& b, cudaStream_t st);
+void launch_stitch(const SectionBatch& child, int child_side, const SectionBatch& parent,
+                   int parent_side, const int* child_offsets, int* child_map,
+                   int connectivity, cudaStream_t st);
+void launch_dense_labels(const int* assign, int npx, int R, int* first, int* rank, int* labels,
+                         cudaStream_t st);
+void launch_graph_init(const SectionBatch& b, const double* counts, const double* sums_rm,
+                       const int64_t* indptr, const int64_t* indices, cudaStream_t st);
+
+}  // namespace rhseg
