@@ -1,0 +1,429 @@
+"""RHSEG throughput bench (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c2|c1|c3b|c5w0|c5w1]
+
+A "step" is one full RHSEG run (every quadtree level, stitching, root labels)
+over one synthetic cube (BASELINE.json configs; SURVEY §8(d) pins the open
+parameters). Metric: pixel-bands/s = edge^2 * bands / step time; spectral
+pairs/s (reference-equivalent, sum over steps of R(R-1)/2 - E) rides along.
+
+ours:      `value` is device time (CUDA events on the run stream) with the cube
+           already resident in HBM; `e2e` is the same metric through the C-ABI
+           host call rhseg_run_host (pinned cube H2D, run, merge log + labels
+           D2H), wall-clocked.
+reference: the CPU restatement of the reference algorithm (oracle/, a C port of
+           rhseg's from-scratch per-step scans, OpenMP over all host threads)
+           timed on a bounded sample of the same workload's leaves; only this
+           leg and `cpu_baseline` touch oracle/.
+
+Multi-GPU (--gpus N under torchrun): the quadtree's leaf level is sharded by
+contiguous subtrees; see paper_2106_12942_b200/distributed.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+# name -> (gen_synthetic args, crop edge or None, levels, weight, target, section_target)
+WORKLOADS = {
+    "c1": ((64, 32, 4, 6, 3.0, 2), None, 1, 0.5, 2, 2),
+    "c2": ((145, 220, 16, 25, 3.0, 145), 144, 3, 0.5, 16, 16),
+    "c3b": ((512, 224, 16, 25, 3.0, 512), None, 5, 0.21, 16, 16),
+    "c4": ((2048, 224, 16, 25, 3.0, 2048), None, 7, 0.21, 16, 16),
+    "c5w0": ((1024, 64, 4, 6, 3.0, 1024), None, 6, 0.0, 16, 16),
+    "c5w1": ((1024, 64, 4, 6, 3.0, 1024), None, 6, 1.0, 16, 16),
+}
+DESCR = {
+    "c1": "C1 gen_synthetic(64,32,4,6,3.0,2) HSEG L=1 w=0.5 t=2",
+    "c2": "C2 gen_synthetic(145,220,16,25,3.0,145).crop(144) RHSEG L=3 w=0.5 t=16",
+    "c3b": "C3 gen_synthetic(512,224,16,25,3.0,512) RHSEG L=5 w=0.21 t=16 (BSMSE twin)",
+    "c4": "C4 gen_synthetic(2048,224,16,25,3.0,2048) RHSEG L=7 w=0.21 t=16",
+    "c5w0": "C5 gen_synthetic(1024,64,4,6,3.0,1024) RHSEG L=6 w=0.0 t=16",
+    "c5w1": "C5 gen_synthetic(1024,64,4,6,3.0,1024) RHSEG L=6 w=1.0 t=16",
+}
+METRIC = "RHSEG pixel-bands/sec"
+UNIT = "pixel-bands/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def make_cube(name, out=None):
+    from paper_2106_12942_b200.synth import gen_synthetic
+
+    spec, crop, *_ = WORKLOADS[name]
+    edge = spec[0]
+    if crop is None:
+        img, _ = gen_synthetic(*spec, out=out)
+        return img.samples
+    full, _ = gen_synthetic(*spec)
+    s = np.ascontiguousarray(full.samples[:, :crop, :crop])
+    if out is not None:
+        out[...] = s
+        return out
+    return s
+
+
+def cube_shape(name):
+    spec, crop, *_ = WORKLOADS[name]
+    e = crop or spec[0]
+    return spec[1], e, e
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the
+    timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the reference algorithm restated in C; test infra only)
+# ---------------------------------------------------------------------------
+def cpu_sample(name, samples, seconds_hint=20.0, threads=None, max_leaves=None, max_steps=-1):
+    """Time whole leaves of the workload (the reference's per-step from-scratch
+    scans; run_leaf, recursive.py:130-142) until ~seconds_hint of CPU work.
+    Upper levels carry <0.01% of the pairs at t=16 and are not
+    sampled; the leaf rate is extrapolated to the whole cube."""
+    from oracle import oracle
+
+    oracle.build()
+    threads = threads or os.cpu_count() or 1
+    oracle.set_threads(threads)
+    spec, crop, levels, w, t, st = WORKLOADS[name]
+    bands, edge, _ = samples.shape
+    side = 1 << (levels - 1)
+    se = edge // side
+    nleaves = side * side
+    leaf_t = t if levels == 1 else st
+    rng = np.random.default_rng(1234)
+    order = rng.permutation(nleaves)
+    done, t0 = 0, time.perf_counter()
+    limit = max_leaves or nleaves
+    while done < limit:
+        k = int(order[done])
+        oracle.run_leaf(samples, (k // side) * se, (k % side) * se, se, w, leaf_t, max_steps=max_steps)
+        done += 1
+        if time.perf_counter() - t0 > seconds_hint:
+            break
+    dt = time.perf_counter() - t0
+    pxb = done * se * se * bands
+    return {
+        "value": pxb / dt,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{done}/{nleaves} random leaves ({se}x{se}x{bands}, {dt:.1f}s) through the C restatement of "
+                  f"rhseg run_leaf/hseg_run (from-scratch scans every step, OpenMP {threads} threads); "
+                  f"pixel-bands/s extrapolated from leaves (upper levels <0.01% of pairs)",
+        "seconds": dt,
+        "leaves": done,
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    name = args.workload
+    samples = make_cube(name)
+    for _ in range(args.warmup):
+        cpu_sample(name, samples, seconds_hint=0.0, max_leaves=1, max_steps=4)
+    vals = []
+    last = None
+    for _ in range(args.steps):
+        last = cpu_sample(name, samples, seconds_hint=args.ref_seconds)
+        vals.append(last["value"])
+    value = float(np.median(vals))
+    bands, edge, _ = samples.shape
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": last["seconds"] * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
+        "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "connectivity": 8,
+                   "parallelism": "cpu-openmp", "l2": "n/a (CPU)"},
+        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import ctypes
+
+    import torch
+
+    import paper_2106_12942_b200 as rh
+    from paper_2106_12942_b200 import _lib
+    from paper_2106_12942_b200.recursive import result_info
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        from paper_2106_12942_b200 import distributed as rdist
+
+        return rdist.bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, cpu_sample)
+
+    name = args.workload
+    spec, crop, levels, w, t, st = WORKLOADS[name]
+    bands, edge, _ = cube_shape(name)
+    host = torch.empty((bands, edge, edge), dtype=torch.float32, pin_memory=True)
+    make_cube(name, out=host.numpy())
+    cube = host.to(dev, non_blocking=False)
+    params = rh.RhsegParams(rh.HsegParams(w, t), levels, st)
+    ex = rh.B200Executor(device=local)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+
+    def step():
+        ctx = ex.execute_device(cube.data_ptr(), edge, bands, params, stream=sptr)
+        return ctx
+
+    for _ in range(max(args.warmup, 0)):
+        ctx = step()
+    torch.cuda.synchronize()
+    info = result_info(ctx)
+    pairs = int(info.spectral_pairs)
+    launches = ctypes.c_int64(0)
+    times, phases, launch_total = [], np.zeros(4), 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            ctx = step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            phases += _phase_ms_of(ctx)
+            lib.rhseg_result_launches(ctx.handle, ctypes.byref(launches))
+            launch_total += int(launches.value)
+    ms = float(np.sum(times)) / args.steps
+    phases /= args.steps
+    npxb = edge * edge * bands
+    value = npxb / (ms * 1e-3)
+
+    # ---- e2e through the C-ABI host call (pinned cube in, log + labels out) ----
+    n_rec = int(info.n_records)
+    oa = torch.empty(max(n_rec, 1), dtype=torch.int32, pin_memory=True)
+    ob = torch.empty(max(n_rec, 1), dtype=torch.int32, pin_memory=True)
+    od = torch.empty(max(n_rec, 1), dtype=torch.float64, pin_memory=True)
+    ok = torch.empty(max(n_rec, 1), dtype=torch.uint8, pin_memory=True)
+    olab = torch.empty(edge * edge, dtype=torch.int32, pin_memory=True)
+    cp = ex.c_params(params)
+    inf2 = _lib.ResultInfoC()
+    hctx = _lib.context(local)
+    e2e_t = []
+    for it in range(2 + args.steps):
+        t0 = time.perf_counter()
+        with hctx.lock:
+            _lib.check(lib.rhseg_run_host(hctx.handle, ctypes.c_void_p(host.data_ptr()), edge, bands,
+                                          ctypes.byref(cp), None, ctypes.c_void_p(oa.data_ptr()),
+                                          ctypes.c_void_p(ob.data_ptr()), ctypes.c_void_p(od.data_ptr()),
+                                          ctypes.c_void_p(ok.data_ptr()), ctypes.c_void_p(olab.data_ptr()),
+                                          ctypes.byref(inf2)), "rhseg_run_host")
+        if it >= 2:
+            e2e_t.append(time.perf_counter() - t0)
+    e2e_s = float(np.median(e2e_t))
+    h2d = edge * edge * bands * 4
+    d2h = n_rec * (4 + 4 + 8 + 1) + edge * edge * 4
+
+    # ---- roofline of the dominant kernel ----
+    roof = roofline(name, edge, bands, levels, w, phases, info, ex, ctx)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
+        "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels,
+                   "spectral_weight": w, "target_regions": t, "connectivity": 8,
+                   "parallelism": "1 GPU, every section of a level concurrent",
+                   "l2": "flushed between timed steps (2x126 MB write)"},
+        "spectral_pairs_per_s": pairs / (ms * 1e-3),
+        "merges": n_rec,
+        "phase_ms": {"init_stitch": phases[0], "dinit_allpairs": phases[1], "merge_loop": phases[2],
+                     "resolve_labels": phases[3]},
+        "gpu_launches": launch_total,
+        "e2e": {"value": npxb / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1e3},
+        "roofline": roof,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        cb = cpu_sample(name, host.numpy(), seconds_hint=args.ref_seconds)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _phase_ms_of(ctx):
+    import ctypes
+
+    from paper_2106_12942_b200 import _lib
+
+    ms = np.zeros(4, np.float32)
+    _lib.check(_lib.load().rhseg_result_phase_ms(ctx.handle, ms.ctypes.data_as(ctypes.c_void_p)), "phase_ms")
+    return ms.astype(np.float64)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
+    """Dominant kernel = the longer of the merge loop (phase 2) and the
+    all-pairs D init (phase 1). Algorithmic work per DESIGN.md §4:
+      dinit (FP64 pipe): sum over sections of R0(R0+1)/2 pairs x (3B+5) ops;
+      merge loop (HBM): per step the row-a pass streams the live regions'
+      fp64 mean vectors once: sum_steps R_live * B * 8 bytes (+ D row/col
+      updates 2*R*8), i.e. ~ sum over sections sum_{R=t+1..R0} R*(8B+16)."""
+    import ctypes
+
+    from paper_2106_12942_b200 import _lib
+
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    side = 1 << (levels - 1)
+    se = edge // side
+    nleaf = side * side
+    R0 = se * se
+    t = WORKLOADS[name][4]
+    loop_ms, dinit_ms = phases[2], phases[1]
+    if loop_ms >= dinit_ms:
+        # leaves dominate (>99% of steps at t=16); count leaf-level steps only
+        per_sec = sum(R * (8 * bands + 16) for R in range(t + 1, R0 + 1))
+        algo = nleaf * per_sec
+        achieved = algo / (loop_ms * 1e-3) / 1e9
+        return {"kernel": "hseg_loop_kernel (persistent per-section merge loop)", "bound": "hbm",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "algorithmic_bytes": algo, "kernel_ms": loop_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    fp64 = ctypes.c_double(0.0)
+    _lib.check(_lib.load().rhseg_fp64_peak(ctx.handle, ctypes.byref(fp64)), "fp64_peak")
+    if w > 0:
+        pairs = nleaf * R0 * (R0 + 1) // 2
+        ops = pairs * (3 * bands + 5)
+    else:
+        ops = 0
+    achieved = ops / (dinit_ms * 1e-3) / 1e12
+    peak = fp64.value / 1e12
+    return {"kernel": "dinit_dense_kernel (all-pairs fp64 dissimilarity)", "bound": "fp64",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+            "traffic": None, "kernel_ms": dinit_ms,
+            "peak_source": "measured live by rhseg_fp64_peak (DSUB+DMUL+DADD issue rate); "
+                           "MEASURED_PEAKS.json has no fp64 figure"}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--ref-seconds", type=float, default=15.0, help="CPU sample budget per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        print("bench.py: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -131,6 +131,9 @@ int rhseg_scan_nonadjacent(int64_t row_start, int64_t row_stop, int64_t col_tile
 /* Per-kernel device time of the last run: [0] leaf/graph init, [1] all-pairs D init,
  * [2] merge loops, [3] stitch+resolve+labels (ms, CUDA events on the run stream). */
 int rhseg_result_phase_ms(rhseg_ctx *ctx, float *ms4);
+/* Kernels this library launched for the last run_* call, plus result copies
+ * (rhseg_result_log) made since (the bench's gpu_launches evidence). */
+int rhseg_result_launches(rhseg_ctx *ctx, int64_t *n);
 /* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure
  * sub/mul/add loop over the whole GPU (roofline denominator). */
 int rhseg_fp64_peak(rhseg_ctx *ctx, double *ops_per_s);

@@ -75,12 +75,13 @@ _SIGS = {
     "rhseg_scan_adjacent": [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp],
     "rhseg_scan_nonadjacent": [i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp],
     "rhseg_result_phase_ms": [vp, vp],
+    "rhseg_result_launches": [vp, vp],
     "rhseg_fp64_peak": [vp, vp],
 }
 EXPORTS = tuple(_SIGS)
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # context() -> Context() -> load() re-enters
 
 
 def load():

@@ -125,6 +125,7 @@ struct rhseg_ctx {
     rhseg_result_info info{};
     float phase_ms[4] = {0, 0, 0, 0};
     bool phases_valid = false;
+    long long launches = 0;  // kernels launched by the last run (+ result copies since)
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -171,6 +172,7 @@ static void reset_ctx(rhseg_ctx* c, cudaStream_t st) {
     c->snap = nullptr;
     c->have = false;
     c->phases_valid = false;
+    c->launches = 0;
     c->evs.clear();
     c->ev_used = 0;
     memset(&c->info, 0, sizeof(c->info));
@@ -277,11 +279,13 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
         {
             PhaseTimer t(c, 1, st);
             launch_dinit(b, n, lv.R0max, st);
+            c->launches += 1;
         }
         CK(cudaGetLastError());
         {
             PhaseTimer t(c, 2, st);
             int e = launch_hseg_loop(b, n, st);
+            c->launches += 1;
             if (e != cudaSuccess)
                 return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
         }
@@ -290,6 +294,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     {
         PhaseTimer t(c, 3, st);
         launch_resolve(lv.sb, st);
+        c->launches += 1;
     }
     CK(cudaGetLastError());
     lv.nlogh.resize(lv.nsec);
@@ -415,6 +420,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         {
             PhaseTimer t(c, 0, st);
             launch_leaf_init(lv.sb, d_samples, edge, side, p->connectivity, st);
+            c->launches += 1;
         }
         CK(cudaGetLastError());
         if (L == 1) {
@@ -447,6 +453,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         {
             PhaseTimer t(c, 0, st);
             launch_stitch(ch.sb, ch.side, pa.sb, pa.side, nullptr, ch.map, p->connectivity, st);
+            c->launches += 1;
         }
         CK(cudaGetLastError());
         free_work(ch, st);
@@ -464,6 +471,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     {
         PhaseTimer t(c, 3, st);
         launch_dense_labels(root.sb.assign, edge * edge, root.Rp, c->lab_first, c->lab_rank, c->labels, st);
+        c->launches += 3;
     }
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
@@ -538,6 +546,12 @@ int rhseg_result_phase_ms(rhseg_ctx* c, float* ms4) {
     return RHSEG_OK;
 }
 
+int rhseg_result_launches(rhseg_ctx* c, int64_t* n) {
+    if (!c || !n) return fail(RHSEG_E_INVALID, "NULL argument");
+    *n = c->launches;
+    return RHSEG_OK;
+}
+
 int rhseg_result_sections(rhseg_ctx* c, int32_t* level, int32_t* row, int32_t* col, int64_t* offset,
                           int64_t* count) {
     if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
@@ -579,6 +593,7 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
         compact_log_kernel<<<lv.nsec, 256, 0, st>>>(lv.sb.log_a, lv.sb.log_b, lv.sb.log_d, lv.sb.log_k, lv.sb.nlog,
                                                     doff, lv.Rp, da + base, db + base, dd + base, dk + base);
         CK(cudaGetLastError());
+        c->launches += 1;
         CK(cudaFreeAsync(doff, st));
         CK(cudaStreamSynchronize(st));  // `off` is reused next level
         base += o;
@@ -702,6 +717,7 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
     {
         PhaseTimer t(c, 0, st);
         launch_graph_init(lv.sb, dc, ds, dp, di, st);
+        c->launches += 1;
     }
     CK(cudaGetLastError());
     CK(cudaFreeAsync(tmp, st));

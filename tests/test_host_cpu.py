@@ -134,3 +134,18 @@ def test_record_list_is_lazy_sequence():
     assert len(rl) == 2 and rl[1].absorbed_id == 3 and rl[1].kind == rh.MergeKind.NON_ADJACENT
     assert rl == [rh.MergeRecord(0, 0, 1, 0.5, rh.MergeKind.ADJACENT),
                   rh.MergeRecord(1, 2, 3, 1.0, rh.MergeKind.NON_ADJACENT)]
+
+
+def test_first_context_call_does_not_deadlock():
+    """_lib.context() as the very first library call (what smoke() does) must
+    reach the device check, not self-deadlock on the module lock."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2106_12942_b200 import _lib, errors\n"
+            "try:\n    _lib.context(0)\nexcept (errors.DeviceError, errors.ExtensionMissing):\n    pass\n"
+            "print('ok')\n") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120,
+                         env={**os.environ, "CUDA_VISIBLE_DEVICES": ""})
+    assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr
