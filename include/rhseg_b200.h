@@ -91,6 +91,33 @@ int rhseg_run_host(rhseg_ctx *ctx, const float *h_samples, int32_t edge, int32_t
                    int32_t *log_absorbed, double *log_dissim, uint8_t *log_kind,
                    int32_t *labels, rhseg_result_info *info);
 
+/* ---- B1 sharded: subtree blocks + reassembly --------------------- */
+/* Levels L..top_level over the block [r0, r0+nr) x [c0, c0+nc) of the level-top
+ * section grid (2^(top-1) sections a side). top_level = 1, block 1x1 is exactly
+ * rhseg_run_device. Each rank of a multi-GPU run owns one block of level-top
+ * subtrees (the quadrant recursion of recursive.py:145-170 below top is local to
+ * it). d_samples is the full cube on this device. */
+int rhseg_run_subtrees(rhseg_ctx *ctx, const float *d_samples, int32_t edge, int32_t bands,
+                       const rhseg_params *params, int32_t top_level, int32_t r0, int32_t c0,
+                       int32_t nr, int32_t nc, void *stream);
+/* Top level of the last run: sections, their region capacity (multiple of 32),
+ * section edge; R0[nsec] initial regions and nlog[nsec] merges (either may be NULL). */
+int rhseg_top_info(rhseg_ctx *ctx, int32_t *nsec, int32_t *rp, int32_t *sec_edge, int32_t *R0,
+                   int32_t *nlog);
+/* Bytes of one packed section state with capacity rp (stitch input, sections.py:103-163):
+ * count u32[rp] | sums f64[rp][bands] | adjacency u32[rp][rp/32] | assignment i32[e*e]. */
+int rhseg_pack_bytes(int32_t rp, int32_t bands, int32_t sec_edge, int64_t *bytes);
+/* Pack the top level's sections (row-major within the block) into a DEVICE buffer
+ * of nsec * rhseg_pack_bytes(rp, ...) bytes, rp >= the level's own capacity. */
+int rhseg_export_top(rhseg_ctx *ctx, int32_t rp, void *d_pack, void *stream);
+/* Rank 0 after the gather: the packed states of ALL 4^(top-1) level-top sections
+ * (row-major over the whole grid) -> stitch + HSEG of levels top-1..1 + root labels.
+ * R0/nlog: host arrays of 4^(top-1) entries. The result covers levels < top_level;
+ * the other levels' logs come from the ranks (rhseg_result_log_device). */
+int rhseg_run_upper(rhseg_ctx *ctx, const void *d_pack, int32_t top_level, int32_t rp,
+                    const int32_t *R0, const int32_t *nlog, int32_t edge, int32_t bands,
+                    const rhseg_params *params, void *stream);
+
 int rhseg_result_info_get(rhseg_ctx *ctx, rhseg_result_info *info);
 /* Sections in log order (level L..1, row-major, recursive.py:95-104): n_sections entries. */
 int rhseg_result_sections(rhseg_ctx *ctx, int32_t *level, int32_t *row, int32_t *col,
@@ -98,6 +125,9 @@ int rhseg_result_sections(rhseg_ctx *ctx, int32_t *level, int32_t *row, int32_t 
 /* Flat merge log, n_records entries each (host buffers). */
 int rhseg_result_log(rhseg_ctx *ctx, int32_t *survivor, int32_t *absorbed, double *dissim,
                      uint8_t *kind);
+/* Same into DEVICE buffers of n_records entries, stream-ordered (for NCCL gathers). */
+int rhseg_result_log_device(rhseg_ctx *ctx, int32_t *survivor, int32_t *absorbed, double *dissim,
+                            uint8_t *kind, void *stream);
 /* labels: dense, first row-major occurrence (graph.py:267-281); assignment: root ids. */
 int rhseg_result_labels(rhseg_ctx *ctx, int32_t *labels, int32_t *assignment);
 /* Root graph state, which = 0: root_initial (pre-root-HSEG, recursive.py:166-167),

@@ -66,6 +66,12 @@ _SIGS = {
     "rhseg_run_device": [vp, vp, i32, i32, ctypes.POINTER(RhsegParamsC), vp],
     "rhseg_run_host": [vp, vp, i32, i32, ctypes.POINTER(RhsegParamsC), vp, vp, vp, vp, vp, vp,
                        ctypes.POINTER(ResultInfoC)],
+    "rhseg_run_subtrees": [vp, vp, i32, i32, ctypes.POINTER(RhsegParamsC), i32, i32, i32, i32, i32, vp],
+    "rhseg_top_info": [vp, vp, vp, vp, vp, vp],
+    "rhseg_pack_bytes": [i32, i32, i32, vp],
+    "rhseg_export_top": [vp, i32, vp, vp],
+    "rhseg_run_upper": [vp, vp, i32, i32, vp, vp, i32, i32, ctypes.POINTER(RhsegParamsC), vp],
+    "rhseg_result_log_device": [vp, vp, vp, vp, vp, vp],
     "rhseg_result_info_get": [vp, ctypes.POINTER(ResultInfoC)],
     "rhseg_result_sections": [vp, vp, vp, vp, vp, vp],
     "rhseg_result_log": [vp, vp, vp, vp, vp],

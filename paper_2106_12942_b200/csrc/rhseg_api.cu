@@ -92,7 +92,11 @@ static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 // one batch of sections (a quadtree level or a standalone graph)
 // ---------------------------------------------------------------------------
 struct Level {
-    int level = 0, side = 0, nsec = 0, edge = 0, Rp = 0, W = 0, C = 1, B = 0, R0max = 0;
+    // the batch is a rows x cols block of this level's side x side section grid
+    // starting at section (row0, col0); a full run covers the whole grid
+    int level = 0, rows = 0, cols = 0, row0 = 0, col0 = 0, nsec = 0, edge = 0, Rp = 0, W = 0, C = 1, B = 0,
+        R0max = 0;
+    bool imported = false;  // state received from other ranks: not part of this ctx's logs
     std::vector<int> R0h, tgth, nlogh, convh;
     std::vector<long long> pairsh;
     SectionBatch sb{};
@@ -110,6 +114,7 @@ struct rhseg_ctx {
     std::vector<Level> levels;  // processing order == log order (L .. 1)
     bool have = false;
     int edge = 0, bands = 0, L = 0;
+    int top = 1;  // highest level processed by the last run (1 = a complete RHSEG with a root)
     // root snapshots (copy 0 of the private per-CTA state)
     void* snap = nullptr;
     uint32_t* init_count = nullptr;
@@ -171,6 +176,7 @@ static void reset_ctx(rhseg_ctx* c, cudaStream_t st) {
     if (c->snap) cudaFreeAsync(c->snap, st);
     c->snap = nullptr;
     c->have = false;
+    c->top = 1;
     c->phases_valid = false;
     c->launches = 0;
     c->evs.clear();
@@ -342,6 +348,7 @@ static void finish_info(rhseg_ctx* c) {
     I.n_sections = 0;
     I.converged_early = 0;
     for (auto& lv : c->levels) {
+        if (lv.imported) continue;
         for (int s = 0; s < lv.nsec; ++s) {
             I.n_records += lv.nlogh[s];
             I.spectral_pairs += lv.pairsh[s];
@@ -349,13 +356,15 @@ static void finish_info(rhseg_ctx* c) {
         }
         I.n_sections += lv.nsec;
     }
-    Level& root = c->levels.back();
     I.levels = c->L;
     I.edge = c->edge;
     I.bands = c->bands;
-    I.root_idspace = root.R0h[0];
-    I.root_initial_regions = c->root_initial_live;
-    I.root_regions = root.R0h[0] - root.nlogh[0];
+    if (c->top == 1) {
+        Level& root = c->levels.back();
+        I.root_idspace = root.R0h[0];
+        I.root_initial_regions = c->root_initial_live;
+        I.root_regions = root.R0h[0] - root.nlogh[0];
+    }
 }
 
 static void finish_phases(rhseg_ctx* c) {
@@ -389,16 +398,86 @@ static int validate(const rhseg_params* p, int edge, int bands) {
     return RHSEG_OK;
 }
 
+// Stitch the back level into its parents and run HSEG on them, level by level,
+// until `stop_level` has been processed (recursive.py:145-170 run_upper_levels).
+static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cudaStream_t st) {
+    const int sect = p->section_target_regions > 0 ? p->section_target_regions : p->target_regions;
+    for (int level = c->levels.back().level - 1; level >= stop_level; --level) {
+        Level& ch = c->levels.back();
+        Level pa;
+        pa.level = level;
+        pa.rows = ch.rows / 2;
+        pa.cols = ch.cols / 2;
+        pa.row0 = ch.row0 / 2;
+        pa.col0 = ch.col0 / 2;
+        pa.nsec = pa.rows * pa.cols;
+        pa.edge = ch.edge * 2;
+        pa.B = c->bands;
+        pa.R0h.assign(pa.nsec, 0);
+        for (int P = 0; P < pa.nsec; ++P) {
+            const int pr = P / pa.cols, pc = P % pa.cols;
+            for (int k = 0; k < 4; ++k) {
+                const int ci = (2 * pr + (k >> 1)) * ch.cols + (2 * pc + (k & 1));
+                pa.R0h[P] += ch.R0h[ci] - ch.nlogh[ci];
+            }
+        }
+        pa.tgth.assign(pa.nsec, level == 1 ? p->target_regions : sect);
+        int rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster);
+        if (rc) return rc;
+        {
+            PhaseTimer t(c, 0, st);
+            launch_stitch(ch.sb, ch.cols, pa.sb, pa.cols, ch.map, p->connectivity, st);
+            c->launches += 1;
+        }
+        CK(cudaGetLastError());
+        if (ch.imported) free_level(ch, st);
+        else free_work(ch, st);
+        c->levels.push_back(std::move(pa));
+        Level& lv = c->levels.back();
+        if (level == 1) {
+            rc = snapshot_root(c, lv, st);
+            if (rc) return rc;
+        }
+        rc = run_level(c, lv, st);
+        if (rc) return rc;
+    }
+    return RHSEG_OK;
+}
+
+static int finish_run(rhseg_ctx* c, cudaStream_t st) {
+    if (c->top == 1) {
+        Level& root = c->levels.back();
+        PhaseTimer t(c, 3, st);
+        launch_dense_labels(root.sb.assign, c->edge * c->edge, root.Rp, c->lab_first, c->lab_rank, c->labels, st);
+        c->launches += 3;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    c->have = true;
+    finish_info(c);
+    finish_phases(c);
+    return RHSEG_OK;
+}
+
+// Levels L..top over the block [r0, r0+nr) x [c0, c0+nc) of the level-`top`
+// section grid; top = 1 with the 1x1 block is SequentialExecutor.execute
+// (recursive.py:173-209). A block of level-`top` subtrees is the unit a rank
+// owns under multi-GPU sharding.
 static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int bands, const rhseg_params* p,
-                           cudaStream_t st) {
+                           int top, int r0, int c0, int nr, int nc, cudaStream_t st) {
     int rc = validate(p, edge, bands);
     if (rc) return rc;
+    const int L = p->levels;
+    if (top < 1 || top > L) return fail(RHSEG_E_INVALID, "top_level must be in [1, levels]");
+    const int tside = 1 << (top - 1);
+    if (nr < 1 || nc < 1 || r0 < 0 || c0 < 0 || r0 + nr > tside || c0 + nc > tside)
+        return fail(RHSEG_E_INVALID, "subtree block outside the level grid");
     CK(cudaSetDevice(c->device));
     reset_ctx(c, st);
     c->edge = edge;
     c->bands = bands;
-    c->L = p->levels;
-    const int L = p->levels;
+    c->L = L;
+    c->top = top;
     const int sect = p->section_target_regions > 0 ? p->section_target_regions : p->target_regions;
     const int side = 1 << (L - 1);
     const int e = edge / side;
@@ -408,9 +487,13 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     {
         c->levels.emplace_back();
         Level& lv = c->levels.back();
+        const int scale = 1 << (L - top);
         lv.level = L;
-        lv.side = side;
-        lv.nsec = side * side;
+        lv.rows = nr * scale;
+        lv.cols = nc * scale;
+        lv.row0 = r0 * scale;
+        lv.col0 = c0 * scale;
+        lv.nsec = lv.rows * lv.cols;
         lv.edge = e;
         lv.B = bands;
         lv.R0h.assign(lv.nsec, e * e);
@@ -419,7 +502,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         if (rc) return rc;
         {
             PhaseTimer t(c, 0, st);
-            launch_leaf_init(lv.sb, d_samples, edge, side, p->connectivity, st);
+            launch_leaf_init(lv.sb, d_samples, edge, lv.cols, lv.row0, lv.col0, p->connectivity, st);
             c->launches += 1;
         }
         CK(cudaGetLastError());
@@ -430,55 +513,30 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         rc = run_level(c, lv, st);
         if (rc) return rc;
     }
-    // ---- upper levels ----
-    for (int level = L - 1; level >= 1; --level) {
-        Level& ch = c->levels.back();
-        Level pa;
-        pa.level = level;
-        pa.side = 1 << (level - 1);
-        pa.nsec = pa.side * pa.side;
-        pa.edge = ch.edge * 2;
-        pa.B = bands;
-        pa.R0h.assign(pa.nsec, 0);
-        for (int P = 0; P < pa.nsec; ++P) {
-            const int pr = P / pa.side, pc = P % pa.side;
-            for (int k = 0; k < 4; ++k) {
-                const int ci = (2 * pr + (k >> 1)) * ch.side + (2 * pc + (k & 1));
-                pa.R0h[P] += ch.R0h[ci] - ch.nlogh[ci];
-            }
-        }
-        pa.tgth.assign(pa.nsec, level == 1 ? p->target_regions : sect);
-        rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster);
-        if (rc) return rc;
-        {
-            PhaseTimer t(c, 0, st);
-            launch_stitch(ch.sb, ch.side, pa.sb, pa.side, nullptr, ch.map, p->connectivity, st);
-            c->launches += 1;
-        }
-        CK(cudaGetLastError());
-        free_work(ch, st);
-        c->levels.push_back(std::move(pa));
-        Level& lv = c->levels.back();
-        if (level == 1) {
-            rc = snapshot_root(c, lv, st);
-            if (rc) return rc;
-        }
-        rc = run_level(c, lv, st);
-        if (rc) return rc;
-    }
-    // ---- dense labels of the root ----
-    Level& root = c->levels.back();
-    {
-        PhaseTimer t(c, 3, st);
-        launch_dense_labels(root.sb.assign, edge * edge, root.Rp, c->lab_first, c->lab_rank, c->labels, st);
-        c->launches += 3;
-    }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-    c->have = true;
-    finish_info(c);
-    finish_phases(c);
-    return RHSEG_OK;
+    rc = upper_levels(c, p, top, st);
+    if (rc) return rc;
+    return finish_run(c, st);
+}
+
+// ---- section state exchange (multi-GPU reassembly) -------------
+// One packed section: count u32[rp] | sums f64[rp][B] | adjacency u32[rp][rp/32]
+// | assignment i32[e*e], each segment 256-byte aligned.
+struct PackLayout {
+    size_t cnt, sums, adj, asg, bytes;
+};
+static PackLayout pack_layout(int rp, int B, int e) {
+    PackLayout P;
+    size_t o = 0;
+    P.cnt = o;
+    o = align256(o + 4 * (size_t)rp);
+    P.sums = o;
+    o = align256(o + 8 * (size_t)rp * B);
+    P.adj = o;
+    o = align256(o + 4 * (size_t)rp * (rp / 32));
+    P.asg = o;
+    o = align256(o + 4 * (size_t)e * e);
+    P.bytes = o;
+    return P;
 }
 
 // ===========================================================================
@@ -530,7 +588,110 @@ int rhseg_run_device(rhseg_ctx* c, const float* d_samples, int32_t edge, int32_t
                      void* stream) {
     if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
-    return run_device_impl(c, d_samples, edge, bands, p, st);
+    return run_device_impl(c, d_samples, edge, bands, p, 1, 0, 0, 1, 1, st);
+}
+
+int rhseg_run_subtrees(rhseg_ctx* c, const float* d_samples, int32_t edge, int32_t bands, const rhseg_params* p,
+                       int32_t top_level, int32_t r0, int32_t c0, int32_t nr, int32_t nc, void* stream) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    return run_device_impl(c, d_samples, edge, bands, p, top_level, r0, c0, nr, nc, st);
+}
+
+int rhseg_top_info(rhseg_ctx* c, int32_t* nsec, int32_t* rp, int32_t* sec_edge, int32_t* R0, int32_t* nlog) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    const Level& lv = c->levels.back();
+    if (nsec) *nsec = lv.nsec;
+    if (rp) *rp = lv.Rp;
+    if (sec_edge) *sec_edge = lv.edge;
+    for (int s = 0; s < lv.nsec; ++s) {
+        if (R0) R0[s] = lv.R0h[s];
+        if (nlog) nlog[s] = lv.nlogh[s];
+    }
+    return RHSEG_OK;
+}
+
+int rhseg_pack_bytes(int32_t rp, int32_t bands, int32_t sec_edge, int64_t* bytes) {
+    if (!bytes || rp < 32 || rp % 32 || bands < 1 || sec_edge < 1) return fail(RHSEG_E_INVALID, "bad pack shape");
+    *bytes = (int64_t)pack_layout(rp, bands, sec_edge).bytes;
+    return RHSEG_OK;
+}
+
+int rhseg_export_top(rhseg_ctx* c, int32_t rp, void* d_pack, void* stream) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    const Level& lv = c->levels.back();
+    if (lv.imported || lv.work == nullptr) return fail(RHSEG_E_STATE, "top level state is not resident");
+    if (rp < lv.Rp || rp % 32) return fail(RHSEG_E_INVALID, "rp must be a multiple of 32 and >= the level's Rp");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    const PackLayout P = pack_layout(rp, lv.B, lv.edge);
+    const size_t B = lv.B, W = lv.W, Wo = rp / 32, npx = (size_t)lv.edge * lv.edge;
+    char* out = static_cast<char*>(d_pack);
+    CK(cudaMemsetAsync(out, 0, P.bytes * lv.nsec, st));
+    for (int s = 0; s < lv.nsec; ++s) {
+        char* o = out + P.bytes * s;
+        const size_t R0 = lv.R0h[s];
+        CK(cudaMemcpyAsync(o + P.cnt, lv.sb.count + (size_t)s * lv.Rp, 4 * R0, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(o + P.sums, lv.sb.sums + (size_t)s * lv.C * lv.sb.sums_copy(), 8 * R0 * B,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpy2DAsync(o + P.adj, 4 * Wo, lv.sb.adj + (size_t)s * lv.C * lv.sb.adj_copy(), 4 * W, 4 * W, R0,
+                             cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(o + P.asg, lv.sb.assign + (size_t)s * npx, 4 * npx, cudaMemcpyDeviceToDevice, st));
+    }
+    return RHSEG_OK;
+}
+
+int rhseg_run_upper(rhseg_ctx* c, const void* d_pack, int32_t top_level, int32_t rp, const int32_t* R0,
+                    const int32_t* nlog, int32_t edge, int32_t bands, const rhseg_params* p, void* stream) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    int rc = validate(p, edge, bands);
+    if (rc) return rc;
+    if (top_level < 2 || top_level > p->levels) return fail(RHSEG_E_INVALID, "top_level must be in [2, levels]");
+    if (rp < 32 || rp % 32) return fail(RHSEG_E_INVALID, "rp must be a positive multiple of 32");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    reset_ctx(c, st);
+    c->edge = edge;
+    c->bands = bands;
+    c->L = p->levels;
+    c->top = 1;
+    const int tside = 1 << (top_level - 1);
+    c->levels.reserve(top_level + 1);
+    c->levels.emplace_back();
+    Level& lv = c->levels.back();
+    lv.level = top_level;
+    lv.rows = lv.cols = tside;
+    lv.nsec = tside * tside;
+    lv.edge = edge / tside;
+    lv.B = bands;
+    lv.imported = true;
+    lv.R0h.assign(R0, R0 + lv.nsec);
+    lv.nlogh.assign(nlog, nlog + lv.nsec);
+    lv.convh.assign(lv.nsec, 0);
+    lv.pairsh.assign(lv.nsec, 0);
+    lv.tgth.assign(lv.nsec, 1);
+    int rpmax = 0;
+    for (int r : lv.R0h) rpmax = std::max(rpmax, r);
+    if (rpmax > rp) return fail(RHSEG_E_INVALID, "a section's R0 exceeds rp");
+    rc = alloc_level(c, lv, p->spectral_weight, st, 1);
+    if (rc) return rc;
+    const PackLayout P = pack_layout(rp, bands, lv.edge);
+    const size_t B = bands, W = lv.W, Wi = rp / 32, npx = (size_t)lv.edge * lv.edge;
+    const char* in = static_cast<const char*>(d_pack);
+    for (int s = 0; s < lv.nsec; ++s) {
+        const char* o = in + P.bytes * s;
+        const size_t r0 = lv.R0h[s];
+        CK(cudaMemcpyAsync(lv.sb.count + (size_t)s * lv.Rp, o + P.cnt, 4 * r0, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(lv.sb.sums + (size_t)s * lv.sb.sums_copy(), o + P.sums, 8 * r0 * B,
+                           cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpy2DAsync(lv.sb.adj + (size_t)s * lv.sb.adj_copy(), 4 * W, o + P.adj, 4 * Wi,
+                             4 * std::min(W, Wi), r0, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(lv.sb.assign + (size_t)s * npx, o + P.asg, 4 * npx, cudaMemcpyDeviceToDevice, st));
+    }
+    lv.done = true;
+    rc = upper_levels(c, p, 1, st);
+    if (rc) return rc;
+    return finish_run(c, st);
 }
 
 int rhseg_result_info_get(rhseg_ctx* c, rhseg_result_info* info) {
@@ -557,15 +718,55 @@ int rhseg_result_sections(rhseg_ctx* c, int32_t* level, int32_t* row, int32_t* c
     if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
     int64_t off = 0;
     int k = 0;
-    for (auto& lv : c->levels)
+    for (auto& lv : c->levels) {
+        if (lv.imported) continue;
         for (int s = 0; s < lv.nsec; ++s, ++k) {
             if (level) level[k] = lv.level;
-            if (row) row[k] = s / lv.side;
-            if (col) col[k] = s % lv.side;
+            if (row) row[k] = lv.row0 + s / lv.cols;
+            if (col) col[k] = lv.col0 + s % lv.cols;
             if (offset) offset[k] = off;
             if (count) count[k] = lv.nlogh[s];
             off += lv.nlogh[s];
         }
+    }
+    return RHSEG_OK;
+}
+
+// Concatenate the per-section device logs in log order (level L..top,
+// row-major) into device arrays of n_records entries.
+static int compact_log(rhseg_ctx* c, int32_t* da, int32_t* db, double* dd, uint8_t* dk, cudaStream_t st) {
+    std::vector<long long> off;
+    std::vector<size_t> first;
+    for (auto& lv : c->levels) {
+        first.push_back(off.size());
+        if (lv.imported) continue;
+        for (int s = 0; s < lv.nsec; ++s) off.push_back(0);
+    }
+    long long base = 0;
+    {
+        size_t k = 0;
+        for (auto& lv : c->levels) {
+            if (lv.imported) continue;
+            for (int s = 0; s < lv.nsec; ++s, ++k) {
+                off[k] = base;
+                base += lv.nlogh[s];
+            }
+        }
+    }
+    if (base == 0) return RHSEG_OK;
+    long long* doff = nullptr;
+    CK(cudaMallocAsync(&doff, 8 * off.size(), st));
+    CK(cudaMemcpyAsync(doff, off.data(), 8 * off.size(), cudaMemcpyHostToDevice, st));
+    for (size_t L = 0; L < c->levels.size(); ++L) {
+        Level& lv = c->levels[L];
+        if (lv.imported) continue;
+        compact_log_kernel<<<lv.nsec, 256, 0, st>>>(lv.sb.log_a, lv.sb.log_b, lv.sb.log_d, lv.sb.log_k, lv.sb.nlog,
+                                                    doff + first[L], lv.Rp, da, db, dd, dk);
+        CK(cudaGetLastError());
+        c->launches += 1;
+    }
+    CK(cudaFreeAsync(doff, st));
+    CK(cudaStreamSynchronize(st));  // `off` must outlive the async H2D copy
     return RHSEG_OK;
 }
 
@@ -575,29 +776,10 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
     int* da = nullptr;
     CK(cudaMallocAsync(&da, (size_t)n * 17 + 1024, st));
     int* db = da + n;
-    double* dd = reinterpret_cast<double*>(db + n);
+    double* dd = reinterpret_cast<double*>(db + n + (n & 1));
     uint8_t* dk = reinterpret_cast<uint8_t*>(dd + n);
-    int64_t base = 0;
-    std::vector<long long> off;
-    long long* doff = nullptr;
-    for (auto& lv : c->levels) {
-        off.resize(lv.nsec);
-        long long o = 0;
-        for (int s = 0; s < lv.nsec; ++s) {
-            off[s] = o;
-            o += lv.nlogh[s];
-        }
-        if (o == 0) continue;
-        CK(cudaMallocAsync(&doff, 8 * (size_t)lv.nsec, st));
-        CK(cudaMemcpyAsync(doff, off.data(), 8 * (size_t)lv.nsec, cudaMemcpyHostToDevice, st));
-        compact_log_kernel<<<lv.nsec, 256, 0, st>>>(lv.sb.log_a, lv.sb.log_b, lv.sb.log_d, lv.sb.log_k, lv.sb.nlog,
-                                                    doff, lv.Rp, da + base, db + base, dd + base, dk + base);
-        CK(cudaGetLastError());
-        c->launches += 1;
-        CK(cudaFreeAsync(doff, st));
-        CK(cudaStreamSynchronize(st));  // `off` is reused next level
-        base += o;
-    }
+    int rc = compact_log(c, da, db, dd, dk, st);
+    if (rc) return rc;
     if (sa) CK(cudaMemcpyAsync(sa, da, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
     if (sb) CK(cudaMemcpyAsync(sb, db, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
     if (sd) CK(cudaMemcpyAsync(sd, dd, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
@@ -605,6 +787,15 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
     CK(cudaFreeAsync(da, st));
     CK(cudaStreamSynchronize(st));
     return RHSEG_OK;
+}
+
+int rhseg_result_log_device(rhseg_ctx* c, int32_t* survivor, int32_t* absorbed, double* dissim, uint8_t* kind,
+                            void* stream) {
+    if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    if (!survivor || !absorbed || !dissim || !kind) return fail(RHSEG_E_INVALID, "NULL device buffer");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
+    return compact_log(c, survivor, absorbed, dissim, kind, st);
 }
 
 int rhseg_result_log(rhseg_ctx* c, int32_t* survivor, int32_t* absorbed, double* dissim, uint8_t* kind) {
@@ -615,6 +806,7 @@ int rhseg_result_log(rhseg_ctx* c, int32_t* survivor, int32_t* absorbed, double*
 
 int rhseg_result_labels(rhseg_ctx* c, int32_t* labels, int32_t* assignment) {
     if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    if (c->top != 1) return fail(RHSEG_E_STATE, "partial (subtree) run has no root labels");
     CK(cudaSetDevice(c->device));
     const size_t npx = (size_t)c->edge * c->edge;
     if (labels) CK(cudaMemcpyAsync(labels, c->labels, npx * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -627,6 +819,7 @@ int rhseg_result_labels(rhseg_ctx* c, int32_t* labels, int32_t* assignment) {
 int rhseg_result_root(rhseg_ctx* c, int32_t which, int64_t* counts, double* sums, uint32_t* adjacency,
                       int32_t* assignment) {
     if (!c || !c->have) return fail(RHSEG_E_STATE, "no result");
+    if (c->top != 1) return fail(RHSEG_E_STATE, "partial (subtree) run has no root graph");
     CK(cudaSetDevice(c->device));
     Level& root = c->levels.back();
     const size_t R = (size_t)root.R0h[0], B = (size_t)root.B, Rp = root.Rp, W = root.W;
@@ -659,7 +852,7 @@ int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t b
     float* d = nullptr;
     CK(cudaMallocAsync(&d, bytes, st));
     CK(cudaMemcpyAsync(d, h_samples, bytes, cudaMemcpyHostToDevice, st));
-    rc = run_device_impl(c, d, edge, bands, p, st);
+    rc = run_device_impl(c, d, edge, bands, p, 1, 0, 0, 1, 1, st);
     cudaFreeAsync(d, st);
     if (rc) return rc;
     rc = copy_log(c, log_survivor, log_absorbed, log_dissim, log_kind, st);
@@ -692,7 +885,7 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
     c->levels.emplace_back();
     Level& lv = c->levels.back();
     lv.level = 1;
-    lv.side = 1;
+    lv.rows = lv.cols = 1;
     lv.nsec = 1;
     lv.edge = 0;
     lv.B = (int)nbands;

@@ -57,12 +57,12 @@ struct SectionBatch {
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
 size_t hseg_loop_smem(int Rp, int C, int B);
-void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int side,
-                      int connectivity, cudaStream_t st);
+void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
+                      int col0, int connectivity, cudaStream_t st);
 void launch_resolve(const SectionBatch& b, cudaStream_t st);
-void launch_stitch(const SectionBatch& child, int child_side, const SectionBatch& parent,
-                   int parent_side, const int* child_offsets, int* child_map,
-                   int connectivity, cudaStream_t st);
+// Parent grid rows x pcols, child grid (2 rows) x (2 pcols), both row-major.
+void launch_stitch(const SectionBatch& child, int child_cols, const SectionBatch& parent,
+                   int parent_cols, int* child_map, int connectivity, cudaStream_t st);
 void launch_dense_labels(const int* assign, int npx, int R, int* first, int* rank, int* labels,
                          cudaStream_t st);
 void launch_graph_init(const SectionBatch& b, const double* counts, const double* sums_rm,

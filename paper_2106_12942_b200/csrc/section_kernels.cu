@@ -14,14 +14,16 @@
 namespace rhseg {
 
 // ---------------------------------------------------------------------------
-// Leaf init: section `sec` of a side x side partition reads its e x e window of
-// the BSQ float32 cube (image.py:59-62 subimage) straight from HBM.
+// Leaf init: section `sec` of a rows x cols block of the leaf grid (origin
+// row0, col0 in sections; the whole side x side partition for a full run)
+// reads its e x e window of the BSQ float32 cube (image.py:59-62 subimage)
+// straight from HBM.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
-leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int side, int conn) {
+leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int cols, int row0, int col0, int conn) {
     const int sec = blockIdx.x;
     const int e = bt.edge, R0 = e * e, B = bt.B, Rp = bt.Rp, W = bt.W;
-    const int orow = (sec / side) * e, ocol = (sec % side) * e;
+    const int orow = (row0 + sec / cols) * e, ocol = (col0 + sec % cols) * e;
     uint32_t* cnt = bt.count + (size_t)sec * Rp;
     int* parent = bt.parent + (size_t)sec * Rp;
     int* assign = bt.assign + (size_t)sec * bt.npx;
@@ -76,10 +78,10 @@ leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int sid
     }
 }
 
-void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int side, int connectivity,
-                      cudaStream_t st) {
+void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0, int col0,
+                      int connectivity, cudaStream_t st) {
     if (b.nsec == 0) return;
-    leaf_init_kernel<<<b.nsec, kThreads, 0, st>>>(b, cube, img_edge, side, connectivity);
+    leaf_init_kernel<<<b.nsec, kThreads, 0, st>>>(b, cube, img_edge, cols, row0, col0, connectivity);
 }
 
 // ---------------------------------------------------------------------------
@@ -128,13 +130,13 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int& total) 
 }
 
 __global__ void __launch_bounds__(kThreads)
-stitch_kernel(SectionBatch ch, int cside, SectionBatch pa, int pside, int* cmap, int conn) {
+stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap, int conn) {
     const int P = blockIdx.x;
-    const int pr = P / pside, pc = P % pside;
+    const int pr = P / pcols, pc = P % pcols;
     const int e = ch.edge, E = pa.edge, B = pa.B;
     __shared__ int scratch[kWarps];
     int cidx[4];
-    for (int k = 0; k < 4; ++k) cidx[k] = (2 * pr + (k >> 1)) * cside + (2 * pc + (k & 1));
+    for (int k = 0; k < 4; ++k) cidx[k] = (2 * pr + (k >> 1)) * ccols + (2 * pc + (k & 1));
     // 1. dense renumber maps
     int base = 0;
     for (int k = 0; k < 4; ++k) {
@@ -224,10 +226,10 @@ stitch_kernel(SectionBatch ch, int cside, SectionBatch pa, int pside, int* cmap,
     }
 }
 
-void launch_stitch(const SectionBatch& child, int child_side, const SectionBatch& parent, int parent_side,
-                   const int* /*child_offsets*/, int* child_map, int connectivity, cudaStream_t st) {
+void launch_stitch(const SectionBatch& child, int child_cols, const SectionBatch& parent, int parent_cols,
+                   int* child_map, int connectivity, cudaStream_t st) {
     if (parent.nsec == 0) return;
-    stitch_kernel<<<parent.nsec, kThreads, 0, st>>>(child, child_side, parent, parent_side, child_map,
+    stitch_kernel<<<parent.nsec, kThreads, 0, st>>>(child, child_cols, parent, parent_cols, child_map,
                                                      connectivity);
 }
 
