@@ -160,12 +160,20 @@ struct Slot {
 };
 static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 
+// Streaming ring for the spectral row-a pass (w > 0): the live regions' mean
+// columns of one CTA are streamed band-chunk by band-chunk from HBM with bulk
+// async copies (TMA 1D) into kStages x kStageBytes of shared memory.
+constexpr int kStages = 4;
+constexpr int kStageBytes = 16 * 1024;
+constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
+
 struct LoopSmem {
-    size_t slot, rslot, pscr, rscr, misc, rpart, mua, bAd, bNd, bAj, bNj, inv, cnt, total;
+    size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B) {
-    const size_t Rs = (size_t)((Rp + C - 1) / C);
+__host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec) {
+    const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
     size_t o = 0;
     L.slot = o;  o += 2 * sizeof(Slot);
@@ -174,6 +182,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B) {
     L.rscr = o;  o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
+    L.bars = o;  o += kStages * 8;
     L.mua = o;   o = align16(o + (size_t)B * 8);
     L.bAd = o;   o = align16(o + Rs * 8);
     L.bNd = o;   o = align16(o + Rs * 8);
@@ -181,72 +190,100 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B) {
     L.bNj = o;   o = align16(o + Rs * 4);
     L.inv = o;   o = align16(o + Rs * 4);
     L.cnt = o;   o = align16(o + (size_t)Rp * 4);
+    L.col = o;   o = align16(o + (spec ? Rs * 4 : 0));
+    L.slot_of = o; o = align16(o + (spec ? Rs * 4 : 0));
+    o = (o + 127) & ~size_t(127);
+    L.ring = o;  o += spec ? (size_t)kStages * kStageBytes : 0;
     L.total = o;
     return L;
 }
-size_t hseg_loop_smem(int Rp, int C, int B) { return loop_smem_layout(Rp, C, B).total; }
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec) { return loop_smem_layout(Rp, C, B, spec).total; }
+int hseg_loop_max_rows() { return kMaxSlots; }
 
 __device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j) {
     if (d < kInf && (d < cd || (d == cd && j < cj))) { cd = d; cj = j; }
 }
 
-// Row-a pass over NQ columns per thread: d(a, j) for own columns j, D row/column
-// update, offer (d, a) to row j's caches, mark rows whose cached partner died.
-template <int NQ, bool SPEC>
-__device__ __forceinline__ void rowa_group(int jbase, int lo, int hi, int a, int b, double nn,
-                                           const double* __restrict__ mu, int Rp, int B,
-                                           const double* mua, const uint32_t* cnt,
-                                           const uint32_t* ra, double* __restrict__ D,
-                                           double* bAd, int* bAj, double* bNd, int* bNj,
-                                           RowBest& pA, RowBest& pN, int* inv, int* ninv) {
+// Epilogue for one column j of the row-a pass: D row/column update, offer
+// (d, a) to row j's caches, mark rows whose cached partner died.
+template <bool SPEC>
+__device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool need, double s, double nn, int a,
+                                         int b, int lo, int Rp, const uint32_t* cnt, double* __restrict__ D,
+                                         double* bAd, int* bAj, double* bNd, int* bNj, RowBest& pA, RowBest& pN,
+                                         int* inv, int* ninv) {
+    if (!valid) return;
+    double d = kInf;
+    if (need) {
+        d = bsmse_finish(nn, (double)cnt[jq], s);
+        D[(size_t)jq * Rp + a] = d;
+        D[(size_t)a * Rp + jq] = d;
+        if (isadj) rb_offer(pA, d, jq);
+        else rb_offer(pN, d, jq);
+    }
+    const int r = jq - lo;
+    int mask = 0;
+    const int ja = bAj[r];
+    if (ja == a || ja == b) mask |= 1;
+    else if (isadj) cache_offer(bAd[r], bAj[r], d, a);
+    if (SPEC) {
+        const int jn = bNj[r];
+        if (jn == a || jn == b) mask |= 2;
+        else if (!isadj) cache_offer(bNd[r], bNj[r], d, a);
+    }
+    if (mask) inv[atomicAdd(ninv, 1)] = (jq << 2) | mask;
+}
+
+// w = 0 row-a pass: only a's neighbours need a dissimilarity (the spectral stage
+// is skipped, engine.py:326), read straight from the band-major mean cache.
+template <int NQ>
+__device__ __forceinline__ void rowa_group_adj(int jbase, int lo, int hi, int a, int b, double nn,
+                                               const double* __restrict__ mu, int Rp, int B, const double* mua,
+                                               const uint32_t* cnt, const uint32_t* ra, double* __restrict__ D,
+                                               double* bAd, int* bAj, RowBest& pA, RowBest& pN, int* inv,
+                                               int* ninv) {
     int j[NQ];
-    bool valid[NQ], isadj[NQ], need[NQ];
+    bool valid[NQ], isadj[NQ];
     double s[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
         j[q] = jbase + q * kThreads;
         valid[q] = j[q] < hi && j[q] != a && j[q] != b && cnt[j[q]] != 0u;
         isadj[q] = valid[q] && ((ra[j[q] >> 5] >> (j[q] & 31)) & 1u);
-        need[q] = valid[q] && (SPEC || isadj[q]);
         s[q] = 0.0;
     }
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) any |= isadj[q];
+    if (any) {
 #pragma unroll 4
-    for (int k = 0; k < B; ++k) {
-        const double m = mua[k];
-        const double* row = mu + (size_t)k * Rp;
+        for (int k = 0; k < B; ++k) {
+            const double m = mua[k];
+            const double* row = mu + (size_t)k * Rp;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            if (need[q]) s[q] = bsmse_step(s[q], m, row[j[q]]);
+            for (int q = 0; q < NQ; ++q)
+                if (isadj[q]) s[q] = bsmse_step(s[q], m, row[j[q]]);
+        }
     }
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        if (!valid[q]) continue;
-        const int jq = j[q];
-        double d = kInf;
-        if (need[q]) {
-            d = bsmse_finish(nn, (double)cnt[jq], s[q]);
-            D[(size_t)jq * Rp + a] = d;
-            D[(size_t)a * Rp + jq] = d;
-            if (isadj[q]) rb_offer(pA, d, jq);
-            else rb_offer(pN, d, jq);
-        }
-        const int r = jq - lo;
-        int mask = 0;
-        const int ja = bAj[r];
-        if (ja == a || ja == b) mask |= 1;
-        else if (isadj[q]) cache_offer(bAd[r], bAj[r], d, a);
-        if (SPEC) {
-            const int jn = bNj[r];
-            if (jn == a || jn == b) mask |= 2;
-            else if (!isadj[q]) cache_offer(bNd[r], bNj[r], d, a);
-        }
-        if (mask) inv[atomicAdd(ninv, 1)] = (jq << 2) | mask;
-    }
+    for (int q = 0; q < NQ; ++q)
+        rowa_col<false>(j[q], valid[q], isadj[q], isadj[q], s[q], nn, a, b, lo, Rp, cnt, D, bAd, bAj, nullptr,
+                        nullptr, pA, pN, inv, ninv);
 }
+
+// Per-CTA streaming state of the spectral row-a pass (all threads hold the same
+// values; only thread 0 issues copies).
+struct StreamState {
+    uint32_t issued;  // stages issued since the kernel started (ring position)
+    int S;            // own compacted columns (ascending ids; holes = -1)
+    int holes;
+    int cur;          // which mean buffer (mu / mu2) holds the compacted columns
+    int S2, KB, nst;  // current step's geometry
+    uint32_t base;    // first stage of the current step
+};
 
 template <bool CLUSTER, bool SPEC>
 __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int C = CLUSTER ? bt.C : 1;
     const int rank = CLUSTER ? (int)cluster_rank() : 0;
     const int sec = bt.sec0 + (int)(blockIdx.x / C);
@@ -254,10 +291,10 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     const int R0 = bt.R0[sec];
     const int B = bt.B, Rp = bt.Rp, W = bt.W;
     const int target = bt.target[sec];
-    const int Rs = (R0 + C - 1) / C;
+    const int Rs = own_rows(R0, C);
     const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
 
-    const LoopSmem L = loop_smem_layout(Rp, C, B);
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -266,7 +303,9 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     int& ninv = misc[0];
     int& sdE = misc[1];
     unsigned long long& sE0 = *reinterpret_cast<unsigned long long*>(misc + 2);
+    int& sScan = misc[4];
     RowBest* rpart = reinterpret_cast<RowBest*>(smem + L.rpart);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
     double* mua = reinterpret_cast<double*>(smem + L.mua);
     double* bAd = reinterpret_cast<double*>(smem + L.bAd);
     double* bNd = reinterpret_cast<double*>(smem + L.bNd);
@@ -274,28 +313,55 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     int* bNj = reinterpret_cast<int*>(smem + L.bNj);
     int* inv = reinterpret_cast<int*>(smem + L.inv);
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
+    int* col = reinterpret_cast<int*>(smem + L.col);
+    int* slot_of = reinterpret_cast<int*>(smem + L.slot_of);
+    double* ring = reinterpret_cast<double*>(smem + L.ring);
 
-    double* __restrict__ mu = bt.mu + sec * bt.mu_stride();
+    double* mubuf[2] = {bt.mu + sec * bt.mu_stride(), SPEC ? bt.mu2 + sec * bt.mu_stride() : nullptr};
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
     uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * bt.adj_copy();
 
-    // Warp-cooperative rescan of one owned row from D (mask bit0: adjacent stage,
-    // bit1: non-adjacent stage) -- the full-row search of _kernels.py restricted to
-    // rows whose cached partner was merged away.
+    // Rescan of one owned row from D (mask bit0: adjacent stage, bit1: non-adjacent
+    // stage) -- the full-row search of _kernels.py restricted to rows whose cached
+    // partner was merged away. Adjacent-only rescans walk the adjacency bitset;
+    // non-adjacent ones stream the D row with 8 loads in flight per lane.
     auto rescan = [&](int i, int mask) {
         RowBest ba = rb_none(), bn = rb_none();
         if (cnt[i] != 0u) {
             const uint32_t* arow = adj + (size_t)i * W;
             const double* drow = D + (size_t)i * Rp;
-            for (int j0 = 0; j0 < R0; j0 += 32) {
-                const int j = j0 + lane;
-                const uint32_t word = arow[j0 >> 5];
-                if (j < R0 && j != i && cnt[j] != 0u) {
-                    if ((word >> lane) & 1u) {
-                        if (mask & 1) rb_offer(ba, __ldcg(drow + j), j);
-                    } else if (SPEC && (mask & 2)) {
-                        rb_offer(bn, __ldcg(drow + j), j);
+            if (!(SPEC && (mask & 2))) {
+                for (int w0 = 0; w0 < W; w0 += 32) {
+                    const int w = w0 + lane;
+                    uint32_t bits = w < W ? arow[w] : 0u;
+                    while (bits) {
+                        const int j = (w << 5) + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        if (j < R0 && cnt[j] != 0u) rb_offer(ba, __ldcg(drow + j), j);
+                    }
+                }
+            } else {
+                for (int j0 = 0; j0 < R0; j0 += 256) {
+                    double dv[8];
+                    uint32_t wv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + 32 * u + lane;
+                        const bool in = j < R0;
+                        dv[u] = in ? __ldcg(drow + j) : kInf;
+                        wv[u] = (j0 + 32 * u) < R0 ? arow[(j0 >> 5) + u] : 0u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int j = j0 + 32 * u + lane;
+                        if (j < R0 && j != i && cnt[j] != 0u) {
+                            if ((wv[u] >> lane) & 1u) {
+                                if (mask & 1) rb_offer(ba, dv[u], j);
+                            } else {
+                                rb_offer(bn, dv[u], j);
+                            }
+                        }
                     }
                 }
             }
@@ -309,12 +375,83 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         }
     };
 
+    // ---- streaming ring (SPEC) ----
+    StreamState ss{};
+    auto issue_stage = [&](uint32_t abs_stage, int i) {  // thread 0 only
+        const int sl = (int)(abs_stage % kStages);
+        const int k0 = i * ss.KB;
+        const int kb = min(ss.KB, B - k0);
+        const uint32_t rowb = (uint32_t)ss.S2 * 8u;
+        fence_proxy_async_shared();
+        mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
+        char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * kStageBytes;
+        const double* src = mubuf[ss.cur] + lo;
+        for (int kk = 0; kk < kb; ++kk) bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
+    };
+    // Block-wide exclusive scan of 0/1 flags (two __syncthreads).
+    auto block_scan = [&](int v, int& total) {
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int* scr = reinterpret_cast<int*>(pscr);
+        if (lane == 31) scr[warp] = x;
+        __syncthreads();
+        int wbase = 0, tot = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            if (w < warp) wbase += scr[w];
+            tot += scr[w];
+        }
+        __syncthreads();
+        total = tot;
+        return wbase + x - v;
+    };
+    // Stable in-place compaction of this CTA's live columns into the other mean
+    // buffer (ids stay ascending, so slot order == id order for every tie-break).
+    auto compact = [&]() {
+        int base = 0;
+        for (int c0 = 0; c0 < ss.S; c0 += kThreads) {
+            const int s = c0 + tid;
+            const int id = s < ss.S ? col[s] : -1;
+            int tot;
+            const int np = base + block_scan(id >= 0 ? 1 : 0, tot);
+            const double* src = mubuf[ss.cur] + lo + s;
+            double* dst = mubuf[ss.cur ^ 1] + lo + np;
+            if (id >= 0) {
+#pragma unroll 8
+                for (int k = 0; k < B; ++k) dst[(size_t)k * Rp] = src[(size_t)k * Rp];
+                slot_of[id - lo] = np;
+            }
+            __syncthreads();  // every read of col[] in this chunk precedes the writes below
+            if (id >= 0) col[np] = id;
+            base += tot;
+        }
+        fence_proxy_async_global();
+        __syncthreads();
+        ss.S = base;
+        ss.holes = 0;
+        ss.cur ^= 1;
+    };
+
     // ---- prologue: counts, per-row caches, initial adjacent-pair count ----
     for (int i = tid; i < Rp; i += kThreads) cnt[i] = i < R0 ? bt.count[(size_t)sec * Rp + i] : 0u;
+    if (SPEC) {
+        for (int r = tid; r < hi - lo; r += kThreads) {
+            col[r] = lo + r;
+            slot_of[r] = r;
+        }
+        ss.S = max(0, hi - lo);
+        if (tid == 0)
+            for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        mbar_init_fence();
+    }
     if (tid == 0) {
         ninv = 0;
         sdE = 0;
         sE0 = 0ull;
+        sScan = 0;
         rpart[0] = rb_none();
         rpart[1] = rb_none();
     }
@@ -333,6 +470,20 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     long long pairs = 0;
     while (R0 - step > target) {
         const int par = step & 1;
+        // (0) spectral stream of this step: compact if >= 25% holes, then put the
+        // first kStages band chunks of the live mean columns in flight. Columns a
+        // and b of this step are never read from the stream.
+        if (SPEC) {
+            if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
+            ss.S2 = (ss.S + 1) & ~1;
+            ss.KB = ss.S2 > 0 ? max(1, min(B, kStageBytes / (ss.S2 * 8))) : B;
+            ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
+            ss.base = ss.issued;
+            const int pre = min(kStages, ss.nst);
+            if (tid == 0)
+                for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
+            ss.issued += pre;
+        }
         // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
         Pair ca = pair_none(), cn = pair_none();
         for (int i = lo + tid; i < hi; i += kThreads) {
@@ -392,7 +543,16 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
             if (N.d < __dmul_rn(bt.weight, da)) { a = N.lo; b = N.hi; dch = N.d; kind = 1; }
         }
         if (a < 0 && hasA) { a = A.lo; b = A.hi; dch = A.d; kind = 0; }
-        if (a < 0) { conv = 1; break; }
+        if (a < 0) {
+            conv = 1;
+            if (SPEC) {  // drain the copies put in flight for this step
+                for (int i = 0; i < min(kStages, ss.nst); ++i) {
+                    const uint32_t g = ss.base + i;
+                    mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
+                }
+            }
+            break;
+        }
 
         // (C) merge (graph.py:229-264) on this CTA's private copies
         const double nn = __dadd_rn((double)cnt[a], (double)cnt[b]);
@@ -400,13 +560,16 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         {
             double* sa = sums + (size_t)a * B;
             const double* sb = sums + (size_t)b * B;
+            double* mu_a = SPEC ? (own_a ? mubuf[ss.cur] + lo + slot_of[a - lo] : nullptr)
+                                : mubuf[0] + a;
             for (int k = tid; k < B; k += kThreads) {
                 const double s = __dadd_rn(sa[k], sb[k]);
                 sa[k] = s;
                 const double m = __ddiv_rn(s, nn);
                 mua[k] = m;
-                if (own_a) mu[(size_t)k * Rp + a] = m;
+                if (own_a) mu_a[(size_t)k * Rp] = m;
             }
+            if (SPEC && own_a) fence_proxy_async_global();
         }
         uint32_t* ra = adj + (size_t)a * W;
         {
@@ -458,20 +621,68 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         __syncthreads();
         if (SPEC) E += sdE;
 
-        // (D) row-a pass over own columns (rows): fresh d(a, j), D update, cache offers
+        // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
-        {
+        if (SPEC) {
+            // columns of this thread: compacted slots tid + 256 q (q < 8)
+            constexpr int NQ = kMaxSlots / kThreads;
+            int jq[NQ];
+            bool valid[NQ], isadj[NQ];
+            double s[NQ];
+            const int nq = (ss.S + kThreads - 1) / kThreads;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int sl = tid + q * kThreads;
+                const int j = (q < nq && sl < ss.S) ? col[sl] : -1;
+                jq[q] = j;
+                valid[q] = j >= 0 && j != a && j != b && cnt[j] != 0u;
+                isadj[q] = valid[q] && ((ra[j >> 5] >> (j & 31)) & 1u);
+                s[q] = 0.0;
+            }
+            for (int i = 0; i < ss.nst; ++i) {
+                const uint32_t g = ss.base + i;
+                mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
+                const double* tile = ring + (size_t)(g % kStages) * (kStageBytes / 8);
+                const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
+                if (nq <= 2) {
+                    for (int kk = 0; kk < kb; ++kk) {
+                        const double m = mua[k0 + kk];
+                        const double* row = tile + (size_t)kk * ss.S2 + tid;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q)
+                            if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
+                    }
+                } else {
+                    for (int kk = 0; kk < kb; ++kk) {
+                        const double m = mua[k0 + kk];
+                        const double* row = tile + (size_t)kk * ss.S2 + tid;
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q)
+                            if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
+                    }
+                }
+                __syncthreads();  // slot g % kStages is free again
+                if (i + kStages < ss.nst) {
+                    if (tid == 0) issue_stage(g + kStages, i + kStages);
+                }
+            }
+            ss.issued += max(0, ss.nst - kStages);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                rowa_col<true>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, D, bAd, bAj, bNd,
+                               bNj, pA, pN, inv, &ninv);
+        } else {
             const int ncols = hi - lo;
+            const double* mu = mubuf[0];
             if (ncols > 2 * kThreads) {
                 for (int jb = lo + tid; jb < hi; jb += 4 * kThreads)
-                    rowa_group<4, SPEC>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
-                                        bNd, bNj, pA, pN, inv, &ninv);
+                    rowa_group_adj<4>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv, &ninv);
             } else if (ncols > kThreads) {
-                rowa_group<2, SPEC>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
-                                    bNd, bNj, pA, pN, inv, &ninv);
+                rowa_group_adj<2>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv,
+                                  &ninv);
             } else {
-                rowa_group<1, SPEC>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj,
-                                    bNd, bNj, pA, pN, inv, &ninv);
+                rowa_group_adj<1>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv,
+                                  &ninv);
             }
         }
         pA = block_min_rb(pA, rscr);
@@ -482,7 +693,12 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
             if (SPEC) sdE = 0;
             cnt[a] = (uint32_t)nn;
             cnt[b] = 0u;
+            if (SPEC && b >= lo && b < hi) {  // b's column becomes a hole of the stream
+                col[slot_of[b - lo]] = -1;
+                slot_of[b - lo] = -1;
+            }
         }
+        if (SPEC && b >= lo && b < hi) ss.holes += 1;
         __syncthreads();
 
         // (E) rescan rows whose cached partner was a or b
@@ -505,7 +721,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
 
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
-    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B);
+    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0);
     void (*kern)(SectionBatch);
     if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true> : hseg_loop_kernel<true, false>;
     else kern = b.spec ? hseg_loop_kernel<false, true> : hseg_loop_kernel<false, false>;

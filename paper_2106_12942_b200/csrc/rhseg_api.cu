@@ -201,12 +201,13 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     lv.Rp = std::max(64, (lv.R0max + 63) / 64 * 64);
     lv.W = lv.Rp / 32;
     lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
-    if (hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024) {
-        // grow the cluster until the per-CTA row slice fits shared memory
-        while (lv.C < kMaxCluster && hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024) lv.C *= 2;
-        if (hseg_loop_smem(lv.Rp, lv.C, lv.B) > 220 * 1024)
-            return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
-    }
+    const bool spec = weight > 0.0;
+    auto fits = [&](int C) {
+        return hseg_loop_smem(lv.Rp, C, lv.B, spec) <= 220 * 1024 && (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
+    };
+    // grow the cluster until the per-CTA row slice fits shared memory
+    while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
+    if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
@@ -226,7 +227,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     o = 0;
     const size_t oAdj = take(ns * C * Rp * W * 4);
     lv.work_zero = o;
-    const size_t oMu = take(ns * B * Rp * 8), oSums = take(ns * C * Rp * B * 8);
+    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec ? ns * B * Rp * 8 : 0),
+                 oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
     CK(cudaMallocAsync(&lv.work, work_bytes, st));
     CK(cudaMemsetAsync(lv.work, 0, lv.work_zero, st));
@@ -241,7 +243,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.C = lv.C;
     b.edge = lv.edge;
     b.npx = (int)npx;
-    b.spec = weight > 0.0 ? 1 : 0;
+    b.spec = spec ? 1 : 0;
     b.weight = weight;
     b.R0 = reinterpret_cast<int*>(K + oR0);
     b.target = reinterpret_cast<int*>(K + oT);
@@ -257,6 +259,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.pairs = reinterpret_cast<long long*>(K + oPr);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
+    b.mu2 = spec ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
     b.sums = reinterpret_cast<double*>(Wk + oSums);
     lv.map = reinterpret_cast<int*>(K + oMap);
     CK(cudaMemcpyAsync(const_cast<int*>(b.R0), lv.R0h.data(), ns * 4, cudaMemcpyHostToDevice, st));
@@ -776,7 +779,7 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
     int* da = nullptr;
     CK(cudaMallocAsync(&da, (size_t)n * 17 + 1024, st));
     int* db = da + n;
-    double* dd = reinterpret_cast<double*>(db + n + (n & 1));
+    double* dd = reinterpret_cast<double*>(db + n);  // 2n ints: 8-byte aligned
     uint8_t* dk = reinterpret_cast<uint8_t*>(dd + n);
     int rc = compact_log(c, da, db, dd, dk, st);
     if (rc) return rc;

@@ -5,6 +5,8 @@
 // Per section s (all arrays padded to Rp = roundup(R0max, 32) region slots):
 //   count [Rp]          u32   pixel counts (0 = dead)      -- graph.py:86-92 pixel_count
 //   mu    [B][Rp]       f64   band-major mean cache        -- sums/count (Appendix A.3)
+//   mu2   [B][Rp]       f64   ping-pong copy: the merge loop keeps each CTA's live columns
+//                             compacted (ascending ids) in mu / mu2 and streams them
 //   D     [Rp][Rp]      f64   dissimilarity matrix, kept exact for every live pair
 //                             (w > 0) or every adjacent pair (w = 0)
 //   sums  [C][Rp][B]    f64   band sums, one private copy per cluster CTA
@@ -32,6 +34,7 @@ struct SectionBatch {
     const int* R0;       // [nsec] initial live regions
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
     double* mu;
+    double* mu2;         // second mean buffer: the loop kernel compacts live columns into it (w > 0)
     double* D;
     double* sums;
     uint32_t* adj;
@@ -56,7 +59,8 @@ struct SectionBatch {
 // Kernel launchers (hseg_kernels.cu / section_kernels.cu). All stream-ordered.
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
-size_t hseg_loop_smem(int Rp, int C, int B);
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec);
+int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
                       int col0, int connectivity, cudaStream_t st);
 void launch_resolve(const SectionBatch& b, cudaStream_t st);
