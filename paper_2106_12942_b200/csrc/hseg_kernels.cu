@@ -182,7 +182,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.rscr = o;  o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
-    L.bars = o;  o += kStages * 8;
+    L.bars = o;  o += 2 * kStages * 8;  // full[kStages], empty[kStages]
     L.mua = o;   o = align16(o + (size_t)B * 8);
     L.bAd = o;   o = align16(o + Rs * 8);
     L.bNd = o;   o = align16(o + Rs * 8);
@@ -305,7 +305,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     unsigned long long& sE0 = *reinterpret_cast<unsigned long long*>(misc + 2);
     int& sScan = misc[4];
     RowBest* rpart = reinterpret_cast<RowBest*>(smem + L.rpart);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);  // full: bulk bytes landed
+    uint64_t* ebars = bars + kStages;                                 // empty: all warps read the slot
     double* mua = reinterpret_cast<double*>(smem + L.mua);
     double* bAd = reinterpret_cast<double*>(smem + L.bAd);
     double* bNd = reinterpret_cast<double*>(smem + L.bNd);
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
         const uint32_t rowb = (uint32_t)ss.S2 * 8u;
+        if (abs_stage >= (uint32_t)kStages) mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
         fence_proxy_async_shared();
         mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
         char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * kStageBytes;
@@ -435,6 +437,20 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         ss.cur ^= 1;
     };
 
+    // Geometry of the next step's stream + its first kStages band chunks in flight
+    // (compacting first when >= 25% of the own columns are holes).
+    auto begin_stream = [&]() {
+        if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
+        ss.S2 = (ss.S + 1) & ~1;
+        ss.KB = ss.S2 > 0 ? max(1, min(B, kStageBytes / (ss.S2 * 8))) : B;
+        ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
+        ss.base = ss.issued;
+        const int pre = min(kStages, ss.nst);
+        if (tid == 0)
+            for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
+        ss.issued += pre;
+    };
+
     // ---- prologue: counts, per-row caches, initial adjacent-pair count ----
     for (int i = tid; i < Rp; i += kThreads) cnt[i] = i < R0 ? bt.count[(size_t)sec * Rp + i] : 0u;
     if (SPEC) {
@@ -444,7 +460,10 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         }
         ss.S = max(0, hi - lo);
         if (tid == 0)
-            for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+            for (int s = 0; s < kStages; ++s) {
+                mbar_init(&bars[s], 1);
+                mbar_init(&ebars[s], kWarps);
+            }
         mbar_init_fence();
     }
     if (tid == 0) {
@@ -465,25 +484,15 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     }
     __syncthreads();
     if (SPEC) E = (long long)(sE0 / 2);
+    if (SPEC && R0 > target) begin_stream();
 
     int a_prev = -1, step = 0, conv = 0;
     long long pairs = 0;
     while (R0 - step > target) {
         const int par = step & 1;
-        // (0) spectral stream of this step: compact if >= 25% holes, then put the
-        // first kStages band chunks of the live mean columns in flight. Columns a
-        // and b of this step are never read from the stream.
-        if (SPEC) {
-            if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
-            ss.S2 = (ss.S + 1) & ~1;
-            ss.KB = ss.S2 > 0 ? max(1, min(B, kStageBytes / (ss.S2 * 8))) : B;
-            ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
-            ss.base = ss.issued;
-            const int pre = min(kStages, ss.nst);
-            if (tid == 0)
-                for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
-            ss.issued += pre;
-        }
+        // (0) the spectral stream of this step was put in flight at the end of the
+        // previous step (or in the prologue); columns a and b of this step are never
+        // read from it.
         // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
         Pair ca = pair_none(), cn = pair_none();
         for (int i = lo + tid; i < hi; i += kThreads) {
@@ -661,7 +670,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                             if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
                     }
                 }
-                __syncthreads();  // slot g % kStages is free again
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ebars[g % kStages]);  // this warp is done with the slot
                 if (i + kStages < ss.nst) {
                     if (tid == 0) issue_stage(g + kStages, i + kStages);
                 }
@@ -700,6 +710,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         }
         if (SPEC && b >= lo && b < hi) ss.holes += 1;
         __syncthreads();
+        // next step's stream overlaps the rescans below and the next argmin
+        if (SPEC && R0 - (step + 1) > target) begin_stream();
 
         // (E) rescan rows whose cached partner was a or b
         const int ni = ninv;
