@@ -318,7 +318,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
     int* slot_of = reinterpret_cast<int*>(smem + L.slot_of);
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
-    double* mubuf[2] = {bt.mu + sec * bt.mu_stride(), SPEC ? bt.mu2 + sec * bt.mu_stride() : nullptr};
+    double* const mu0 = bt.mu + sec * bt.mu_stride();
+    double* const mu1 = SPEC ? bt.mu2 + sec * bt.mu_stride() : nullptr;
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
     uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * bt.adj_copy();
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         fence_proxy_async_shared();
         mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
         char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * kStageBytes;
-        const double* src = mubuf[ss.cur] + lo;
+        const double* src = (ss.cur ? mu1 : mu0) + lo;
         for (int kk = 0; kk < kb; ++kk) bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
     };
     // Block-wide exclusive scan of 0/1 flags (two __syncthreads).
@@ -419,8 +420,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
             const int id = s < ss.S ? col[s] : -1;
             int tot;
             const int np = base + block_scan(id >= 0 ? 1 : 0, tot);
-            const double* src = mubuf[ss.cur] + lo + s;
-            double* dst = mubuf[ss.cur ^ 1] + lo + np;
+            const double* src = (ss.cur ? mu1 : mu0) + lo + s;
+            double* dst = (ss.cur ? mu0 : mu1) + lo + np;
             if (id >= 0) {
 #pragma unroll 8
                 for (int k = 0; k < B; ++k) dst[(size_t)k * Rp] = src[(size_t)k * Rp];
@@ -569,8 +570,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         {
             double* sa = sums + (size_t)a * B;
             const double* sb = sums + (size_t)b * B;
-            double* mu_a = SPEC ? (own_a ? mubuf[ss.cur] + lo + slot_of[a - lo] : nullptr)
-                                : mubuf[0] + a;
+            double* mu_a = SPEC ? (own_a ? (ss.cur ? mu1 : mu0) + lo + slot_of[a - lo] : nullptr)
+                                : mu0 + a;
             for (int k = tid; k < B; k += kThreads) {
                 const double s = __dadd_rn(sa[k], sb[k]);
                 sa[k] = s;
@@ -683,7 +684,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                                bNj, pA, pN, inv, &ninv);
         } else {
             const int ncols = hi - lo;
-            const double* mu = mubuf[0];
+            const double* mu = mu0;
             if (ncols > 2 * kThreads) {
                 for (int jb = lo + tid; jb < hi; jb += 4 * kThreads)
                     rowa_group_adj<4>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv, &ninv);
