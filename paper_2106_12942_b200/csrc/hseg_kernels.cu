@@ -489,6 +489,16 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
 
     int a_prev = -1, step = 0, conv = 0;
     long long pairs = 0;
+    // optional per-phase cycle accounting (RHSEG_PROFILE=1): thread 0 of every CTA
+    unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+    long long tmark = clock64();
+    auto mark = [&](int ph) {
+        if (bt.prof && tid == 0) {
+            const long long t = clock64();
+            pc[ph] += (unsigned long long)(t - tmark);
+            tmark = t;
+        }
+    };
     while (R0 - step > target) {
         const int par = step & 1;
         // (0) the spectral stream of this step was put in flight at the end of the
@@ -514,6 +524,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         if (CLUSTER) cluster_barrier();
         else __syncthreads();
 
+        mark(0);
         // (B) combine the C slots: identical decision in every CTA
         if (CLUSTER) {
             if (tid < C * 16) {
@@ -564,6 +575,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
             break;
         }
 
+        mark(1);
         // (C) merge (graph.py:229-264) on this CTA's private copies
         const double nn = __dadd_rn((double)cnt[a], (double)cnt[b]);
         const bool own_a = a >= lo && a < hi;
@@ -631,6 +643,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         __syncthreads();
         if (SPEC) E += sdE;
 
+        mark(2);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
         if (SPEC) {
@@ -714,10 +727,12 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         // next step's stream overlaps the rescans below and the next argmin
         if (SPEC && R0 - (step + 1) > target) begin_stream();
 
+        mark(3);
         // (E) rescan rows whose cached partner was a or b
         const int ni = ninv;
         for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3);
         __syncthreads();
+        mark(4);
         a_prev = a;
         ++step;
     }
@@ -726,6 +741,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         for (int i = tid; i < Rp; i += kThreads) bt.count[(size_t)sec * Rp + i] = cnt[i];
         if (tid == 0) {
             bt.nlog[sec] = step;
+            if (bt.prof)
+                for (int q = 0; q < 5; ++q) atomicAdd(bt.prof + q, pc[q]);
             bt.conv[sec] = conv;
             if (bt.pairs) bt.pairs[sec] = pairs;
         }

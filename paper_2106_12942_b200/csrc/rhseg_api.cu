@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -267,7 +269,26 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     return RHSEG_OK;
 }
 // dinit + merge loop over D-sized chunks of sections, then union-find resolve.
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static bool profiling() {
+    static const bool on = [] {
+        const char* e = getenv("RHSEG_PROFILE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
 static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
+    unsigned long long* prof = nullptr;
+    if (profiling()) {
+        CK(cudaMallocAsync(&prof, 8 * 8, st));
+        CK(cudaMemsetAsync(prof, 0, 8 * 8, st));
+    }
+    lv.sb.prof = prof;
+    const double t_enter = prof ? now_ms() : 0.0;
     const size_t dsec = (size_t)lv.Rp * lv.Rp * 8;
     size_t freeb = 0, totalb = 0;
     CK(cudaMemGetInfo(&freeb, &totalb));
@@ -312,7 +333,21 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     CK(cudaMemcpyAsync(lv.nlogh.data(), lv.sb.nlog, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.convh.data(), lv.sb.conv, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.pairsh.data(), lv.sb.pairs, 8 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
+    unsigned long long ph[8] = {0};
+    if (prof) CK(cudaMemcpyAsync(ph, prof, 8 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (prof) {
+        long long steps = 0;
+        for (int s = 0; s < lv.nsec; ++s) steps += lv.nlogh[s];
+        const double tot = (double)(ph[0] + ph[1] + ph[2] + ph[3] + ph[4]) + 1e-9;
+        fprintf(stderr,
+                "[rhseg profile] level %d: %d sections x C=%d, Rp=%d, %lld steps, %.0f cycles/step/CTA: "
+                "argmin %.1f%% combine %.1f%% merge %.1f%% row-a %.1f%% rescan %.1f%%\n",
+                lv.level, lv.nsec, lv.C, lv.Rp, steps, tot / (double)std::max(1LL, steps) / lv.C,
+                100 * ph[0] / tot, 100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot);
+        cudaFree(prof);
+        fprintf(stderr, "[rhseg profile] level %d host wall in run_level %.2f ms\n", lv.level, now_ms() - t_enter);
+    }
     lv.done = true;
     return RHSEG_OK;
 }
@@ -448,6 +483,7 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
 }
 
 static int finish_run(rhseg_ctx* c, cudaStream_t st) {
+    if (profiling()) fprintf(stderr, "[rhseg profile] finish at %.2f ms\n", now_ms());
     if (c->top == 1) {
         Level& root = c->levels.back();
         PhaseTimer t(c, 3, st);
@@ -476,6 +512,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     if (nr < 1 || nc < 1 || r0 < 0 || c0 < 0 || r0 + nr > tside || c0 + nc > tside)
         return fail(RHSEG_E_INVALID, "subtree block outside the level grid");
     CK(cudaSetDevice(c->device));
+    if (profiling()) fprintf(stderr, "[rhseg profile] run start at %.2f ms\n", now_ms());
     reset_ctx(c, st);
     c->edge = edge;
     c->bands = bands;

@@ -49,6 +49,7 @@ struct SectionBatch {
     int* conv;
     long long* pairs;    // [nsec] reference-equivalent spectral pairs, sum_steps R(R-1)/2 - E
     int sec0;            // first section covered by D (D is allocated per launch chunk)
+    unsigned long long* prof;  // [5] per-phase cycles summed over CTAs (nullptr = off)
 
     __host__ __device__ size_t mu_stride() const { return (size_t)B * Rp; }
     __host__ __device__ size_t d_stride() const { return (size_t)Rp * Rp; }
