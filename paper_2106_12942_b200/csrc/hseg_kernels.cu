@@ -166,6 +166,7 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 constexpr int kStages = 4;
 constexpr int kStageBytes = 16 * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
+constexpr int kPrefetchBytes = 192 * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
     size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, ring, total;
@@ -278,6 +279,7 @@ struct StreamState {
     int holes;
     int cur;          // which mean buffer (mu / mu2) holds the compacted columns
     int S2, KB, nst;  // current step's geometry
+    int pf, PF;       // next band row to prefetch into L2 / prefetch distance in rows
     uint32_t base;    // first stage of the current step
 };
 
@@ -379,17 +381,28 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
 
     // ---- streaming ring (SPEC) ----
     StreamState ss{};
-    auto issue_stage = [&](uint32_t abs_stage, int i) {  // thread 0 only
+    // Stage `i` of the current step into ring slot abs_stage % kStages. Called by
+    // all lanes of warp 0: lane 0 arms the full barrier, the lanes issue one bulk
+    // copy per band row in parallel, and rows kPrefetch bytes further ahead are
+    // prefetched into L2 so the next stages' copies hit L2 instead of HBM.
+    auto issue_stage = [&](uint32_t abs_stage, int i) {
         const int sl = (int)(abs_stage % kStages);
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
         const uint32_t rowb = (uint32_t)ss.S2 * 8u;
         if (abs_stage >= (uint32_t)kStages) mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
-        fence_proxy_async_shared();
-        mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
+        if (lane == 0) {
+            fence_proxy_async_shared();
+            mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
+        }
+        __syncwarp();
         char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * kStageBytes;
         const double* src = (ss.cur ? mu1 : mu0) + lo;
-        for (int kk = 0; kk < kb; ++kk) bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
+        for (int kk = lane; kk < kb; kk += 32)
+            bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
+        const int p0 = max(k0 + kb, ss.pf), p1 = min(B, k0 + kb + ss.PF);
+        for (int k = p0 + lane; k < p1; k += 32) bulk_prefetch_l2(src + (size_t)k * Rp, rowb);
+        ss.pf = max(ss.pf, p1);
     };
     // Block-wide exclusive scan of 0/1 flags (two __syncthreads).
     auto block_scan = [&](int v, int& total) {
@@ -446,8 +459,10 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         ss.KB = ss.S2 > 0 ? max(1, min(B, kStageBytes / (ss.S2 * 8))) : B;
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
+        ss.pf = 0;
+        ss.PF = ss.S2 > 0 ? min(B, max(1, kPrefetchBytes / (ss.S2 * 8))) : 0;
         const int pre = min(kStages, ss.nst);
-        if (tid == 0)
+        if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
         ss.issued += pre;
     };
@@ -687,7 +702,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ebars[g % kStages]);  // this warp is done with the slot
                 if (i + kStages < ss.nst) {
-                    if (tid == 0) issue_stage(g + kStages, i + kStages);
+                    if (warp == 0) issue_stage(g + kStages, i + kStages);
                 }
             }
             ss.issued += max(0, ss.nst - kStages);
