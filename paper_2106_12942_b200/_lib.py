@@ -16,7 +16,7 @@ import numpy as np
 from .errors import DeviceError, ExtensionMissing, IndivisibleImage
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "_lib", "librhseg_b200.so")
+LIB_PATH = os.environ.get("RHSEG_LIB_PATH") or os.path.join(PKG, "_lib", "librhseg_b200.so")
 
 RHSEG_OK = 0
 RHSEG_E_INVALID = 1

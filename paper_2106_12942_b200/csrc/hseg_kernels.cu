@@ -163,10 +163,25 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // Streaming ring for the spectral row-a pass (w > 0): the live regions' mean
 // columns of one CTA are streamed band-chunk by band-chunk from HBM with bulk
 // async copies (TMA 1D) into kStages x kStageBytes of shared memory.
-constexpr int kStages = 4;
-constexpr int kStageBytes = 16 * 1024;
+#ifndef RHSEG_STAGES
+#define RHSEG_STAGES 4
+#endif
+#ifndef RHSEG_STAGE_KB
+#define RHSEG_STAGE_KB 16
+#endif
+#ifndef RHSEG_PREFETCH_KB
+#define RHSEG_PREFETCH_KB 0
+#endif
+#ifndef RHSEG_EMPTY_BARRIERS
+#define RHSEG_EMPTY_BARRIERS 0
+#endif
+#ifndef RHSEG_EARLY_STREAM
+#define RHSEG_EARLY_STREAM 1
+#endif
+constexpr int kStages = RHSEG_STAGES;
+constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
-constexpr int kPrefetchBytes = 192 * 1024;  // L2 prefetch distance of the stream per CTA
+constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
     size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, ring, total;
@@ -390,7 +405,8 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
         const uint32_t rowb = (uint32_t)ss.S2 * 8u;
-        if (abs_stage >= (uint32_t)kStages) mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
+        if (RHSEG_EMPTY_BARRIERS && abs_stage >= (uint32_t)kStages)
+            mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
         if (lane == 0) {
             fence_proxy_async_shared();
             mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
@@ -400,9 +416,11 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         const double* src = (ss.cur ? mu1 : mu0) + lo;
         for (int kk = lane; kk < kb; kk += 32)
             bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
-        const int p0 = max(k0 + kb, ss.pf), p1 = min(B, k0 + kb + ss.PF);
-        for (int k = p0 + lane; k < p1; k += 32) bulk_prefetch_l2(src + (size_t)k * Rp, rowb);
-        ss.pf = max(ss.pf, p1);
+        if (kPrefetchBytes > 0) {
+            const int p0 = max(k0 + kb, ss.pf), p1 = min(B, k0 + kb + ss.PF);
+            for (int k = p0 + lane; k < p1; k += 32) bulk_prefetch_l2(src + (size_t)k * Rp, rowb);
+            ss.pf = max(ss.pf, p1);
+        }
     };
     // Block-wide exclusive scan of 0/1 flags (two __syncthreads).
     auto block_scan = [&](int v, int& total) {
@@ -460,7 +478,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
         ss.pf = 0;
-        ss.PF = ss.S2 > 0 ? min(B, max(1, kPrefetchBytes / (ss.S2 * 8))) : 0;
+        ss.PF = (ss.S2 > 0 && kPrefetchBytes > 0) ? min(B, max(1, kPrefetchBytes / (ss.S2 * 8))) : 0;
         const int pre = min(kStages, ss.nst);
         if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
@@ -699,8 +717,12 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                             if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
                     }
                 }
+#if RHSEG_EMPTY_BARRIERS
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&ebars[g % kStages]);  // this warp is done with the slot
+#else
+                __syncthreads();  // slot g % kStages is free again
+#endif
                 if (i + kStages < ss.nst) {
                     if (warp == 0) issue_stage(g + kStages, i + kStages);
                 }
@@ -740,7 +762,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         if (SPEC && b >= lo && b < hi) ss.holes += 1;
         __syncthreads();
         // next step's stream overlaps the rescans below and the next argmin
-        if (SPEC && R0 - (step + 1) > target) begin_stream();
+        if (RHSEG_EARLY_STREAM && SPEC && R0 - (step + 1) > target) begin_stream();
 
         mark(3);
         // (E) rescan rows whose cached partner was a or b
@@ -750,6 +772,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         mark(4);
         a_prev = a;
         ++step;
+        if (!RHSEG_EARLY_STREAM && SPEC && R0 - step > target) begin_stream();
     }
     if (CLUSTER) cluster_barrier();  // keep our slots alive until every peer is done reading
     if (rank == 0) {
