@@ -163,17 +163,27 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // Streaming ring for the spectral row-a pass (w > 0): the live regions' mean
 // columns of one CTA are streamed band-chunk by band-chunk from HBM with bulk
 // async copies (TMA 1D) into kStages x kStageBytes of shared memory.
+// Measured on C4 (tools/ab_variants.py, profiles/r01_loop_variants.md): 2 x 32 KB
+// stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
+// per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
+// per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
 #ifndef RHSEG_STAGES
-#define RHSEG_STAGES 4
+#define RHSEG_STAGES 2
 #endif
 #ifndef RHSEG_STAGE_KB
-#define RHSEG_STAGE_KB 16
+#define RHSEG_STAGE_KB 32
 #endif
 #ifndef RHSEG_PREFETCH_KB
 #define RHSEG_PREFETCH_KB 0
 #endif
 #ifndef RHSEG_EMPTY_BARRIERS
 #define RHSEG_EMPTY_BARRIERS 0
+#endif
+#ifndef RHSEG_DIRECT
+#define RHSEG_DIRECT 0
+#endif
+#ifndef RHSEG_UNROLL
+#define RHSEG_UNROLL 8
 #endif
 #ifndef RHSEG_EARLY_STREAM
 #define RHSEG_EARLY_STREAM 1
@@ -209,7 +219,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.col = o;   o = align16(o + (spec ? Rs * 4 : 0));
     L.slot_of = o; o = align16(o + (spec ? Rs * 4 : 0));
     o = (o + 127) & ~size_t(127);
-    L.ring = o;  o += spec ? (size_t)kStages * kStageBytes : 0;
+    L.ring = o;  o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * kStageBytes + kThreads * 8 : 0;  // + overrun pad
     L.total = o;
     return L;
 }
@@ -298,8 +308,11 @@ struct StreamState {
     uint32_t base;    // first stage of the current step
 };
 
+#ifndef RHSEG_MINBLOCKS
+#define RHSEG_MINBLOCKS 2
+#endif
 template <bool CLUSTER, bool SPEC>
-__global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
+__global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = CLUSTER ? bt.C : 1;
     const int rank = CLUSTER ? (int)cluster_rank() : 0;
@@ -479,7 +492,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         ss.base = ss.issued;
         ss.pf = 0;
         ss.PF = (ss.S2 > 0 && kPrefetchBytes > 0) ? min(B, max(1, kPrefetchBytes / (ss.S2 * 8))) : 0;
-        const int pre = min(kStages, ss.nst);
+        const int pre = RHSEG_DIRECT ? 0 : min(kStages, ss.nst);
         if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
         ss.issued += pre;
@@ -600,7 +613,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
         if (a < 0) {
             conv = 1;
             if (SPEC) {  // drain the copies put in flight for this step
-                for (int i = 0; i < min(kStages, ss.nst); ++i) {
+                for (int i = 0; i < (RHSEG_DIRECT ? 0 : min(kStages, ss.nst)); ++i) {
                     const uint32_t g = ss.base + i;
                     mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
                 }
@@ -695,27 +708,57 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                 isadj[q] = valid[q] && ((ra[j >> 5] >> (j & 31)) & 1u);
                 s[q] = 0.0;
             }
+#if RHSEG_DIRECT
+            {
+                // direct coalesced loads of the compacted columns, RHSEG_UNROLL bands in
+                // flight per thread (no shared-memory staging, no block barriers)
+                const double* base = (ss.cur ? mu1 : mu0) + lo + tid;
+                switch (nq) {
+#define RHSEG_DIRECT_NQ(NQC, U)                                                              \
+    case NQC: {                                                                              \
+        bool ok[NQC];                                                                        \
+        _Pragma("unroll") for (int q = 0; q < NQC; ++q) ok[q] = tid + q * kThreads < ss.S;   \
+        for (int k0 = 0; k0 < B; k0 += U) {                                                  \
+            double v[U][NQC];                                                                \
+            _Pragma("unroll") for (int u = 0; u < U; ++u)                                    \
+                _Pragma("unroll") for (int q = 0; q < NQC; ++q)                              \
+                    v[u][q] = (ok[q] && k0 + u < B) ? __ldcs(base + (size_t)(k0 + u) * Rp + q * kThreads) : 0.0; \
+            _Pragma("unroll") for (int u = 0; u < U; ++u) {                                  \
+                if (k0 + u < B) {                                                            \
+                    const double m = mua[k0 + u];                                            \
+                    _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = bsmse_step(s[q], m, v[u][q]); \
+                }                                                                            \
+            }                                                                                \
+        }                                                                                    \
+    } break;
+                    RHSEG_DIRECT_NQ(1, RHSEG_UNROLL) RHSEG_DIRECT_NQ(2, RHSEG_UNROLL)
+                    RHSEG_DIRECT_NQ(3, RHSEG_UNROLL) RHSEG_DIRECT_NQ(4, RHSEG_UNROLL)
+                    RHSEG_DIRECT_NQ(5, 4) RHSEG_DIRECT_NQ(6, 4) RHSEG_DIRECT_NQ(7, 4) RHSEG_DIRECT_NQ(8, 4)
+#undef RHSEG_DIRECT_NQ
+                    default: break;
+                }
+            }
+#else
             for (int i = 0; i < ss.nst; ++i) {
                 const uint32_t g = ss.base + i;
                 mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
                 const double* tile = ring + (size_t)(g % kStages) * (kStageBytes / 8);
                 const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
-                if (nq <= 2) {
-                    for (int kk = 0; kk < kb; ++kk) {
-                        const double m = mua[k0 + kk];
-                        const double* row = tile + (size_t)kk * ss.S2 + tid;
-#pragma unroll
-                        for (int q = 0; q < 2; ++q)
-                            if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
-                    }
-                } else {
-                    for (int kk = 0; kk < kb; ++kk) {
-                        const double m = mua[k0 + kk];
-                        const double* row = tile + (size_t)kk * ss.S2 + tid;
-#pragma unroll
-                        for (int q = 0; q < NQ; ++q)
-                            if (valid[q]) s[q] = bsmse_step(s[q], m, row[q * kThreads]);
-                    }
+                // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
+                // accumulate garbage that the epilogue discards via valid[])
+                switch (nq) {
+#define RHSEG_CONSUME(NQC)                                                        \
+    case NQC:                                                                     \
+        for (int kk = 0; kk < kb; ++kk) {                                         \
+            const double m = mua[k0 + kk];                                        \
+            const double* row = tile + (size_t)kk * ss.S2 + tid;                  \
+            _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = bsmse_step(s[q], m, row[q * kThreads]); \
+        }                                                                         \
+        break;
+                    RHSEG_CONSUME(1) RHSEG_CONSUME(2) RHSEG_CONSUME(3) RHSEG_CONSUME(4)
+                    RHSEG_CONSUME(5) RHSEG_CONSUME(6) RHSEG_CONSUME(7) RHSEG_CONSUME(8)
+#undef RHSEG_CONSUME
+                    default: break;
                 }
 #if RHSEG_EMPTY_BARRIERS
                 __syncwarp();
@@ -728,6 +771,7 @@ __global__ void __launch_bounds__(kThreads) hseg_loop_kernel(SectionBatch bt) {
                 }
             }
             ss.issued += max(0, ss.nst - kStages);
+#endif
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 rowa_col<true>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, D, bAd, bAj, bNd,
