@@ -273,6 +273,17 @@ static double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+static bool profiling();
+static double g_t0 = 0.0;
+#define RHSEG_TRACE(...)                                                          \
+    do {                                                                          \
+        if (profiling()) {                                                        \
+            fprintf(stderr, "[rhseg trace] %8.3f ms  ", now_ms() - g_t0);         \
+            fprintf(stderr, __VA_ARGS__);                                         \
+            fputc('\n', stderr);                                                  \
+        }                                                                         \
+    } while (0)
+
 static bool profiling() {
     static const bool on = [] {
         const char* e = getenv("RHSEG_PROFILE");
@@ -291,7 +302,9 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     const double t_enter = prof ? now_ms() : 0.0;
     const size_t dsec = (size_t)lv.Rp * lv.Rp * 8;
     size_t freeb = 0, totalb = 0;
+    RHSEG_TRACE("run_level %d: enter", lv.level);
     CK(cudaMemGetInfo(&freeb, &totalb));
+    RHSEG_TRACE("run_level %d: meminfo", lv.level);
     size_t budget = (size_t)(0.6 * (double)(freeb + c->dmat_bytes));
     size_t chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, budget / dsec));
     if (c->dmat_bytes < chunk * dsec) {
@@ -327,6 +340,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
         c->launches += 1;
     }
     CK(cudaGetLastError());
+    RHSEG_TRACE("run_level %d: launched", lv.level);
     lv.nlogh.resize(lv.nsec);
     lv.convh.resize(lv.nsec);
     lv.pairsh.resize(lv.nsec);
@@ -336,6 +350,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     unsigned long long ph[8] = {0};
     if (prof) CK(cudaMemcpyAsync(ph, prof, 8 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    RHSEG_TRACE("run_level %d: synced", lv.level);
     if (prof) {
         long long steps = 0;
         for (int s = 0; s < lv.nsec; ++s) steps += lv.nlogh[s];
@@ -460,7 +475,9 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
             }
         }
         pa.tgth.assign(pa.nsec, level == 1 ? p->target_regions : sect);
+        RHSEG_TRACE("level %d: alloc", level);
         int rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster);
+        RHSEG_TRACE("level %d: alloc done", level);
         if (rc) return rc;
         {
             PhaseTimer t(c, 0, st);
@@ -483,7 +500,7 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
 }
 
 static int finish_run(rhseg_ctx* c, cudaStream_t st) {
-    if (profiling()) fprintf(stderr, "[rhseg profile] finish at %.2f ms\n", now_ms());
+    RHSEG_TRACE("finish");
     if (c->top == 1) {
         Level& root = c->levels.back();
         PhaseTimer t(c, 3, st);
@@ -512,8 +529,10 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     if (nr < 1 || nc < 1 || r0 < 0 || c0 < 0 || r0 + nr > tside || c0 + nc > tside)
         return fail(RHSEG_E_INVALID, "subtree block outside the level grid");
     CK(cudaSetDevice(c->device));
-    if (profiling()) fprintf(stderr, "[rhseg profile] run start at %.2f ms\n", now_ms());
+    g_t0 = now_ms();
+    RHSEG_TRACE("run start");
     reset_ctx(c, st);
+    RHSEG_TRACE("reset done");
     c->edge = edge;
     c->bands = bands;
     c->L = L;
@@ -538,7 +557,9 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         lv.B = bands;
         lv.R0h.assign(lv.nsec, e * e);
         lv.tgth.assign(lv.nsec, L == 1 ? p->target_regions : sect);
+        RHSEG_TRACE("leaves: alloc");
         rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster);
+        RHSEG_TRACE("leaves: alloc done");
         if (rc) return rc;
         {
             PhaseTimer t(c, 0, st);
