@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // stage) -- the full-row search of _kernels.py restricted to rows whose cached
     // partner was merged away. Adjacent-only rescans walk the adjacency bitset;
     // non-adjacent ones stream the D row with 8 loads in flight per lane.
+    StreamState ss{};
     auto rescan = [&](int i, int mask) {
         RowBest ba = rb_none(), bn = rb_none();
         if (cnt[i] != 0u) {
@@ -373,6 +374,32 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                         if (j < R0 && cnt[j] != 0u) rb_offer(ba, __ldcg(drow + j), j);
                     }
                 }
+            } else if (!CLUSTER) {
+                // one CTA owns every column: walk the compacted live-column list
+                // (ascending ids, holes = -1), 16 D loads in flight per lane
+                constexpr int U = 16;
+                for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                    double dv[U];
+                    int jv[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int sl = s0 + 32 * u + lane;
+                        const int j = sl < ss.S ? col[sl] : -1;
+                        jv[u] = j;
+                        dv[u] = j >= 0 ? __ldcs(drow + j) : kInf;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = jv[u];
+                        if (j >= 0 && j != i && cnt[j] != 0u) {
+                            if ((arow[j >> 5] >> (j & 31)) & 1u) {
+                                if (mask & 1) rb_offer(ba, dv[u], j);
+                            } else {
+                                rb_offer(bn, dv[u], j);
+                            }
+                        }
+                    }
+                }
             } else {
                 for (int j0 = 0; j0 < R0; j0 += 256) {
                     double dv[8];
@@ -381,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     for (int u = 0; u < 8; ++u) {
                         const int j = j0 + 32 * u + lane;
                         const bool in = j < R0;
-                        dv[u] = in ? __ldcg(drow + j) : kInf;
+                        dv[u] = in ? __ldcs(drow + j) : kInf;
                         wv[u] = (j0 + 32 * u) < R0 ? arow[(j0 >> 5) + u] : 0u;
                     }
 #pragma unroll
@@ -408,7 +435,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     };
 
     // ---- streaming ring (SPEC) ----
-    StreamState ss{};
     // Stage `i` of the current step into ring slot abs_stage % kStages. Called by
     // all lanes of warp 0: lane 0 arms the full barrier, the lanes issue one bulk
     // copy per band row in parallel, and rows kPrefetch bytes further ahead are
