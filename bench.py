@@ -37,15 +37,19 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 # name -> (gen_synthetic args, crop edge or None, levels, weight, target, section_target)
+# measure: MEASURE_OF (default sqrt-bsmse, the reference's only measure)
 WORKLOADS = {
     "c1": ((64, 32, 4, 6, 3.0, 2), None, 1, 0.5, 2, 2),
+    "c3": ((512, 224, 16, 25, 3.0, 512), None, 5, 0.21, 16, 16),
     "c2": ((145, 220, 16, 25, 3.0, 145), 144, 3, 0.5, 16, 16),
     "c3b": ((512, 224, 16, 25, 3.0, 512), None, 5, 0.21, 16, 16),
     "c4": ((2048, 224, 16, 25, 3.0, 2048), None, 7, 0.21, 16, 16),
     "c5w0": ((1024, 64, 4, 6, 3.0, 1024), None, 6, 0.0, 16, 16),
     "c5w1": ((1024, 64, 4, 6, 3.0, 1024), None, 6, 1.0, 16, 16),
 }
+MEASURE_OF = {"c3": "sam"}
 DESCR = {
+    "c3": "C3 gen_synthetic(512,224,16,25,3.0,512) RHSEG L=5 SAM w=0.21 t=16 (extension measure)",
     "c1": "C1 gen_synthetic(64,32,4,6,3.0,2) HSEG L=1 w=0.5 t=2",
     "c2": "C2 gen_synthetic(145,220,16,25,3.0,145).crop(144) RHSEG L=3 w=0.5 t=16",
     "c3b": "C3 gen_synthetic(512,224,16,25,3.0,512) RHSEG L=5 w=0.21 t=16 (BSMSE twin)",
@@ -149,6 +153,7 @@ def cpu_sample(name, samples, seconds_hint=20.0, threads=None, max_leaves=None, 
     oracle.build()
     threads = threads or os.cpu_count() or 1
     oracle.set_threads(threads)
+    oracle.set_measure(MEASURE_OF.get(name, "sqrt-bsmse"))
     spec, crop, levels, w, t, st = WORKLOADS[name]
     bands, edge, _ = samples.shape
     side = 1 << (levels - 1)
@@ -246,7 +251,7 @@ def run_ours(args):
     host = torch.empty((bands, edge, edge), dtype=torch.float32, pin_memory=True)
     make_cube(name, out=host.numpy())
     cube = host.to(dev, non_blocking=False)
-    params = rh.RhsegParams(rh.HsegParams(w, t), levels, st)
+    params = rh.RhsegParams(rh.HsegParams(w, t, MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
     ex = rh.B200Executor(device=local)
     stream = torch.cuda.Stream(device=dev)  # the run and its events share one non-default stream
     sptr = stream.cuda_stream
@@ -329,6 +334,7 @@ def run_ours(args):
         "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
         "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels,
                    "spectral_weight": w, "target_regions": t, "connectivity": 8,
+                   "measure": MEASURE_OF.get(name, "sqrt-bsmse"),
                    "parallelism": "1 GPU, every section of a level concurrent",
                    "l2": "flushed between timed steps (2x126 MB write)"},
         "spectral_pairs_per_s": pairs / (ms * 1e-3),

@@ -55,7 +55,9 @@ typedef struct {
     int32_t section_target_regions; /* >= 1; every section above the root (0 = target) */
     int32_t levels;                 /* >= 1 recursion levels */
     int32_t connectivity;           /* 4 or 8 */
-    int32_t measure;                /* 0 = "sqrt-bsmse" (the only reference measure, dissim.py:45) */
+    int32_t measure;                /* 0 = "sqrt-bsmse" (the reference's only measure, dissim.py:45);
+                                       1 = "euclidean", 2 = "sam" (north-star extensions, same fp64
+                                       conventions; parity pinned to the oracle only) */
     int32_t cluster;                /* 0 = auto; else CTAs per section in {1,2,4,8,16} */
 } rhseg_params;
 
@@ -143,7 +145,7 @@ int rhseg_result_root(rhseg_ctx *ctx, int32_t which, int64_t *counts, double *su
 int rhseg_hseg_graph(rhseg_ctx *ctx, int64_t n, int64_t nbands, const double *counts,
                      const double *sums, const int64_t *indptr, const int64_t *indices,
                      double spectral_weight, int64_t target_regions, int32_t cluster,
-                     int32_t *log_survivor, int32_t *log_absorbed, double *log_dissim,
+                     int32_t measure, int32_t *log_survivor, int32_t *log_absorbed, double *log_dissim,
                      uint8_t *log_kind, int64_t *n_records, int32_t *converged_early);
 
 /* ---- B3: per-row best-partner tables (_kernels.py:31-115), HOST buffers --------- */

@@ -46,6 +46,10 @@ def lib():
         L.oracle_run_leaf.restype = i64
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_set_threads.restype = None
+        L.oracle_set_measure.argtypes = [ctypes.c_int]
+        L.oracle_set_measure.restype = None
+        L.oracle_acos.argtypes = [ctypes.c_double]
+        L.oracle_acos.restype = ctypes.c_double
         _lib = L
     return _lib
 
@@ -56,6 +60,19 @@ def _p(a):
 
 def set_threads(n: int) -> None:
     lib().oracle_set_threads(int(n))
+
+
+MEASURE_CODES = {"sqrt-bsmse": 0, "euclidean": 1, "sam": 2}
+
+
+def set_measure(name: str) -> None:
+    """Dissimilarity for every following call (process-wide): "sqrt-bsmse"
+    (the reference's), or the extensions "euclidean" / "sam"."""
+    lib().oracle_set_measure(MEASURE_CODES[name])
+
+
+def acos(x: float) -> float:
+    return lib().oracle_acos(float(x))
 
 
 def scan_adjacent(row_start, row_stop, counts, sums, indptr, indices, out_d, out_j):

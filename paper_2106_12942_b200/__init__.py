@@ -6,7 +6,7 @@ Drop-in entry points (same names, arguments and results as the reference):
   rhseg_run / B200Executor.execute -> RhsegResult                          (recursive)
 """
 
-from .dissim import MEASURES, resolve_measure, sqrt_bsmse
+from .dissim import MEASURES, acos_fdlibm, euclidean, resolve_measure, sam, sqrt_bsmse
 from .engine import (
     BestPairTable,
     GraphSnapshot,

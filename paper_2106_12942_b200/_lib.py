@@ -77,7 +77,7 @@ _SIGS = {
     "rhseg_result_log": [vp, vp, vp, vp, vp],
     "rhseg_result_labels": [vp, vp, vp],
     "rhseg_result_root": [vp, i32, vp, vp, vp, vp],
-    "rhseg_hseg_graph": [vp, i64, i64, vp, vp, vp, vp, f64, i64, i32, vp, vp, vp, vp, vp, vp],
+    "rhseg_hseg_graph": [vp, i64, i64, vp, vp, vp, vp, f64, i64, i32, i32, vp, vp, vp, vp, vp, vp],
     "rhseg_scan_adjacent": [i64, i64, i64, i64, vp, vp, vp, vp, vp, vp],
     "rhseg_scan_nonadjacent": [i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp],
     "rhseg_result_phase_ms": [vp, vp],

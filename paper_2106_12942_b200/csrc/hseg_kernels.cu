@@ -38,6 +38,7 @@ namespace rhseg {
 constexpr int kTile = 64;
 constexpr int kKB = 16;
 
+template <int M>
 __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) {
     const int sec = bt.sec0 + blockIdx.y;
     const int R0 = bt.R0[sec];
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     const double* __restrict__ mu = bt.mu + sec * bt.mu_stride();
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     const uint32_t* __restrict__ cnt = bt.count + (size_t)sec * Rp;
+    const double* __restrict__ n2 = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
 
     // band staging (sA, sB) and the transpose tile (sT) share one buffer: sT is
     // only touched after the last band chunk's trailing __syncthreads().
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[p][q] = bsmse_step(acc[p][q], a[p], b[q]);
+                for (int q = 0; q < 4; ++q) acc[p][q] = acc_step<M>(acc[p][q], a[p], b[q]);
         }
         __syncthreads();
     }
@@ -97,7 +99,8 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
             const int j = j0 + tx + 16 * q;
             double d = 0.0;
             if (i < R0 && j < R0) {
-                d = bsmse_finish((double)cnt[i], (double)cnt[j], acc[p][q]);
+                d = pair_finish<M>((double)cnt[i], (double)cnt[j], acc[p][q], M == kSam ? n2[i] : 0.0,
+                                   M == kSam ? n2[j] : 0.0);
                 D[(size_t)i * Rp + j] = d;
             }
             sT[ty + 16 * p][tx + 16 * q] = d;
@@ -113,6 +116,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
 
 // w = 0: only adjacent pairs are ever read (engine.py:326 skips the spectral stage),
 // so D is filled on the adjacency graph only. One thread per row.
+template <int M>
 __global__ void __launch_bounds__(kThreads) dinit_sparse_kernel(SectionBatch bt) {
     const int sec = bt.sec0 + blockIdx.y;
     const int R0 = bt.R0[sec];
@@ -131,8 +135,10 @@ __global__ void __launch_bounds__(kThreads) dinit_sparse_kernel(SectionBatch bt)
             bits &= bits - 1;
             if (j <= i) continue;
             double s = 0.0;
-            for (int k = 0; k < B; ++k) s = bsmse_step(s, mu[(size_t)k * Rp + i], mu[(size_t)k * Rp + j]);
-            const double d = bsmse_finish((double)cnt[i], (double)cnt[j], s);
+            for (int k = 0; k < B; ++k) s = acc_step<M>(s, mu[(size_t)k * Rp + i], mu[(size_t)k * Rp + j]);
+            const double* n2 = bt.nrm2 + (size_t)sec * Rp;
+            const double d = pair_finish<M>((double)cnt[i], (double)cnt[j], s, M == kSam ? n2[i] : 0.0,
+                                            M == kSam ? n2[j] : 0.0);
             D[(size_t)i * Rp + j] = d;
             D[(size_t)j * Rp + i] = d;
         }
@@ -144,10 +150,14 @@ void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st) {
     if (b.spec) {
         const int nt = (R0max + kTile - 1) / kTile;
         dim3 grid(nt * (nt + 1) / 2, nrun);
-        dinit_dense_kernel<<<grid, kThreads, 0, st>>>(b);
+        if (b.measure == kSam) dinit_dense_kernel<kSam><<<grid, kThreads, 0, st>>>(b);
+        else if (b.measure == kEuclid) dinit_dense_kernel<kEuclid><<<grid, kThreads, 0, st>>>(b);
+        else dinit_dense_kernel<kBsmse><<<grid, kThreads, 0, st>>>(b);
     } else {
         dim3 grid((R0max + kThreads - 1) / kThreads, nrun);
-        dinit_sparse_kernel<<<grid, kThreads, 0, st>>>(b);
+        if (b.measure == kSam) dinit_sparse_kernel<kSam><<<grid, kThreads, 0, st>>>(b);
+        else if (b.measure == kEuclid) dinit_sparse_kernel<kEuclid><<<grid, kThreads, 0, st>>>(b);
+        else dinit_sparse_kernel<kBsmse><<<grid, kThreads, 0, st>>>(b);
     }
 }
 
@@ -232,15 +242,16 @@ __device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j
 
 // Epilogue for one column j of the row-a pass: D row/column update, offer
 // (d, a) to row j's caches, mark rows whose cached partner died.
-template <bool SPEC>
+template <bool SPEC, int M>
 __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool need, double s, double nn, int a,
-                                         int b, int lo, int Rp, const uint32_t* cnt, double* __restrict__ D,
+                                         int b, int lo, int Rp, const uint32_t* cnt, double n2a,
+                                         const double* __restrict__ n2, double* __restrict__ D,
                                          double* bAd, int* bAj, double* bNd, int* bNj, RowBest& pA, RowBest& pN,
                                          int* inv, int* ninv) {
     if (!valid) return;
     double d = kInf;
     if (need) {
-        d = bsmse_finish(nn, (double)cnt[jq], s);
+        d = pair_finish<M>(nn, (double)cnt[jq], s, n2a, M == kSam ? n2[jq] : 0.0);
         D[(size_t)jq * Rp + a] = d;
         D[(size_t)a * Rp + jq] = d;
         if (isadj) rb_offer(pA, d, jq);
@@ -261,10 +272,11 @@ __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool ne
 
 // w = 0 row-a pass: only a's neighbours need a dissimilarity (the spectral stage
 // is skipped, engine.py:326), read straight from the band-major mean cache.
-template <int NQ>
+template <int NQ, int M>
 __device__ __forceinline__ void rowa_group_adj(int jbase, int lo, int hi, int a, int b, double nn,
                                                const double* __restrict__ mu, int Rp, int B, const double* mua,
-                                               const uint32_t* cnt, const uint32_t* ra, double* __restrict__ D,
+                                               const uint32_t* cnt, const uint32_t* ra, double n2a,
+                                               const double* __restrict__ n2, double* __restrict__ D,
                                                double* bAd, int* bAj, RowBest& pA, RowBest& pN, int* inv,
                                                int* ninv) {
     int j[NQ];
@@ -287,13 +299,13 @@ __device__ __forceinline__ void rowa_group_adj(int jbase, int lo, int hi, int a,
             const double* row = mu + (size_t)k * Rp;
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
-                if (isadj[q]) s[q] = bsmse_step(s[q], m, row[j[q]]);
+                if (isadj[q]) s[q] = acc_step<M>(s[q], m, row[j[q]]);
         }
     }
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
-        rowa_col<false>(j[q], valid[q], isadj[q], isadj[q], s[q], nn, a, b, lo, Rp, cnt, D, bAd, bAj, nullptr,
-                        nullptr, pA, pN, inv, ninv);
+        rowa_col<false, M>(j[q], valid[q], isadj[q], isadj[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2, D, bAd, bAj,
+                           nullptr, nullptr, pA, pN, inv, ninv);
 }
 
 // Per-CTA streaming state of the spectral row-a pass (all threads hold the same
@@ -311,7 +323,7 @@ struct StreamState {
 #ifndef RHSEG_MINBLOCKS
 #define RHSEG_MINBLOCKS 2
 #endif
-template <bool CLUSTER, bool SPEC>
+template <bool CLUSTER, bool SPEC, int M>
 __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = CLUSTER ? bt.C : 1;
@@ -351,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     double* const mu0 = bt.mu + sec * bt.mu_stride();
     double* const mu1 = SPEC ? bt.mu2 + sec * bt.mu_stride() : nullptr;
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
     uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * bt.adj_copy();
 
@@ -718,6 +731,16 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         mark(2);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
+        double n2a = 0.0;
+        if (M == kSam) {  // squared norm of a's new mean, sequential (oracle order)
+            double* sn2a = reinterpret_cast<double*>(misc + 6);
+            if (tid == 0) {
+                *sn2a = norm2_seq(mua, 1, B);
+                if (own_a) n2g[a] = *sn2a;
+            }
+            __syncthreads();
+            n2a = *sn2a;
+        }
         if (SPEC) {
             // columns of this thread: compacted slots tid + 256 q (q < 8)
             constexpr int NQ = kMaxSlots / kThreads;
@@ -752,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             _Pragma("unroll") for (int u = 0; u < U; ++u) {                                  \
                 if (k0 + u < B) {                                                            \
                     const double m = mua[k0 + u];                                            \
-                    _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = bsmse_step(s[q], m, v[u][q]); \
+                    _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, v[u][q]); \
                 }                                                                            \
             }                                                                                \
         }                                                                                    \
@@ -778,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         for (int kk = 0; kk < kb; ++kk) {                                         \
             const double m = mua[k0 + kk];                                        \
             const double* row = tile + (size_t)kk * ss.S2 + tid;                  \
-            _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = bsmse_step(s[q], m, row[q * kThreads]); \
+            _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, row[q * kThreads]); \
         }                                                                         \
         break;
                     RHSEG_CONSUME(1) RHSEG_CONSUME(2) RHSEG_CONSUME(3) RHSEG_CONSUME(4)
@@ -800,20 +823,21 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #endif
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
-                rowa_col<true>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, D, bAd, bAj, bNd,
-                               bNj, pA, pN, inv, &ninv);
+                rowa_col<true, M>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2g, D, bAd,
+                                  bAj, bNd, bNj, pA, pN, inv, &ninv);
         } else {
             const int ncols = hi - lo;
             const double* mu = mu0;
             if (ncols > 2 * kThreads) {
                 for (int jb = lo + tid; jb < hi; jb += 4 * kThreads)
-                    rowa_group_adj<4>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv, &ninv);
+                    rowa_group_adj<4, M>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA, pN,
+                                         inv, &ninv);
             } else if (ncols > kThreads) {
-                rowa_group_adj<2>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv,
-                                  &ninv);
+                rowa_group_adj<2, M>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA,
+                                     pN, inv, &ninv);
             } else {
-                rowa_group_adj<1>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, D, bAd, bAj, pA, pN, inv,
-                                  &ninv);
+                rowa_group_adj<1, M>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA,
+                                     pN, inv, &ninv);
             }
         }
         pA = block_min_rb(pA, rscr);
@@ -861,8 +885,17 @@ int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
     const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0);
     void (*kern)(SectionBatch);
-    if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true> : hseg_loop_kernel<true, false>;
-    else kern = b.spec ? hseg_loop_kernel<false, true> : hseg_loop_kernel<false, false>;
+#define RHSEG_PICK(M)                                                                              \
+    if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true, M> : hseg_loop_kernel<true, false, M>; \
+    else kern = b.spec ? hseg_loop_kernel<false, true, M> : hseg_loop_kernel<false, false, M>;
+    if (b.measure == kSam) {
+        RHSEG_PICK(kSam)
+    } else if (b.measure == kEuclid) {
+        RHSEG_PICK(kEuclid)
+    } else {
+        RHSEG_PICK(kBsmse)
+    }
+#undef RHSEG_PICK
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (b.C > 8) {

@@ -99,6 +99,7 @@ struct Level {
     int level = 0, rows = 0, cols = 0, row0 = 0, col0 = 0, nsec = 0, edge = 0, Rp = 0, W = 0, C = 1, B = 0,
         R0max = 0;
     bool imported = false;  // state received from other ranks: not part of this ctx's logs
+    int measure = 0;        // 0 sqrt-bsmse, 1 euclidean, 2 sam
     std::vector<int> R0h, tgth, nlogh, convh;
     std::vector<long long> pairsh;
     SectionBatch sb{};
@@ -222,7 +223,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     const size_t oR0 = take(ns * 4), oT = take(ns * 4), oCnt = take(ns * Rp * 4), oPar = take(ns * Rp * 4),
                  oAs = take(ns * npx * 4), oMap = take(ns * Rp * 4), oLa = take(ns * Rp * 4),
                  oLb = take(ns * Rp * 4), oLd = take(ns * Rp * 8), oLk = take(ns * Rp), oN = take(ns * 4),
-                 oCv = take(ns * 4), oPr = take(ns * 8);
+                 oCv = take(ns * 4), oPr = take(ns * 8), oN2 = take(lv.measure == 2 ? ns * Rp * 8 : 0);
     const size_t keep_bytes = o;
     CK(cudaMallocAsync(&lv.keep, keep_bytes, st));
     CK(cudaMemsetAsync(lv.keep, 0, keep_bytes, st));
@@ -246,6 +247,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.edge = lv.edge;
     b.npx = (int)npx;
     b.spec = spec ? 1 : 0;
+    b.measure = lv.measure;
+    b.nrm2 = lv.measure == 2 ? reinterpret_cast<double*>(K + oN2) : nullptr;
     b.weight = weight;
     b.R0 = reinterpret_cast<int*>(K + oR0);
     b.target = reinterpret_cast<int*>(K + oT);
@@ -438,7 +441,8 @@ static int validate(const rhseg_params* p, int edge, int bands) {
     if (p->section_target_regions < 0) return fail(RHSEG_E_INVALID, "section_target_regions must be >= 1");
     if (p->levels < 1) return fail(RHSEG_E_INVALID, "levels must be >= 1");
     if (p->connectivity != 4 && p->connectivity != 8) return fail(RHSEG_E_INVALID, "connectivity must be 4 or 8");
-    if (p->measure != 0) return fail(RHSEG_E_INVALID, "unknown measure; available: ['sqrt-bsmse']");
+    if (p->measure < 0 || p->measure > 2)
+        return fail(RHSEG_E_INVALID, "unknown measure; available: ['euclidean', 'sam', 'sqrt-bsmse']");
     if (edge < 1 || bands < 1) return fail(RHSEG_E_INVALID, "width and bands must be >= 1");
     if (p->levels > 30) return fail(RHSEG_E_INVALID, "levels too large");
     const long long side = 1LL << (p->levels - 1);
@@ -466,6 +470,7 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
         pa.nsec = pa.rows * pa.cols;
         pa.edge = ch.edge * 2;
         pa.B = c->bands;
+        pa.measure = p->measure;
         pa.R0h.assign(pa.nsec, 0);
         for (int P = 0; P < pa.nsec; ++P) {
             const int pr = P / pa.cols, pc = P % pa.cols;
@@ -555,6 +560,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         lv.nsec = lv.rows * lv.cols;
         lv.edge = e;
         lv.B = bands;
+        lv.measure = p->measure;
         lv.R0h.assign(lv.nsec, e * e);
         lv.tgth.assign(lv.nsec, L == 1 ? p->target_regions : sect);
         RHSEG_TRACE("leaves: alloc");
@@ -725,6 +731,7 @@ int rhseg_run_upper(rhseg_ctx* c, const void* d_pack, int32_t top_level, int32_t
     lv.nsec = tside * tside;
     lv.edge = edge / tside;
     lv.B = bands;
+    lv.measure = p->measure;
     lv.imported = true;
     lv.R0h.assign(R0, R0 + lv.nsec);
     lv.nlogh.assign(nlog, nlog + lv.nsec);
@@ -928,10 +935,13 @@ int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t b
 
 int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* counts, const double* sums,
                      const int64_t* indptr, const int64_t* indices, double weight, int64_t target, int32_t cluster,
+                     int32_t measure,
                      int32_t* log_survivor, int32_t* log_absorbed, double* log_dissim, uint8_t* log_kind,
                      int64_t* n_records, int32_t* converged_early) {
     if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
     if (!(weight >= 0.0 && weight <= 1.0)) return fail(RHSEG_E_INVALID, "spectral_weight must be in [0, 1]");
+    if (measure < 0 || measure > 2)
+        return fail(RHSEG_E_INVALID, "unknown measure; available: ['euclidean', 'sam', 'sqrt-bsmse']");
     if (target < 1) return fail(RHSEG_E_INVALID, "target_regions must be >= 1");
     if (n < 0 || nbands < 1) return fail(RHSEG_E_INVALID, "bad graph shape");
     if (n > 16384) return fail(RHSEG_E_TOO_LARGE, "graph exceeds 16384 regions");
@@ -950,6 +960,7 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
     lv.nsec = 1;
     lv.edge = 0;
     lv.B = (int)nbands;
+    lv.measure = measure;
     lv.R0h.assign(1, (int)n);
     lv.tgth.assign(1, (int)std::min<int64_t>(target, INT32_MAX));
     int rc = alloc_level(c, lv, weight, st, cluster);

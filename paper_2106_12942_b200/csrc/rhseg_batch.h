@@ -30,10 +30,12 @@ struct SectionBatch {
     int edge;      // section edge in pixels (0 for a standalone graph)
     int npx;       // edge * edge
     int spec;      // spectral stage on (weight > 0)
+    int measure;   // 0 sqrt-bsmse (reference), 1 euclidean, 2 sam (extensions)
     double weight; // spectral_weight (engine.py:33)
     const int* R0;       // [nsec] initial live regions
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
     double* mu;
+    double* nrm2;        // [nsec][Rp] squared norm of each mean vector (sam only, else nullptr)
     double* mu2;         // second mean buffer: the loop kernel compacts live columns into it (w > 0)
     double* D;
     double* sums;

@@ -34,6 +34,91 @@ __device__ __forceinline__ double bsmse_finish(double ni, double nj, double s) {
 }
 
 // ---------------------------------------------------------------------------
+// Extension measures (BASELINE north star: BSMSE / SAM / Euclidean). The
+// reference ships only sqrt-bsmse (dissim.py:45); these follow the same
+// conventions (fp64, bands ascending, no FMA) and are pinned only against the
+// oracle's restatement (oracle/rhseg_oracle.c), i.e. parity unpinned.
+//   euclidean: d = sqrt(sum_b (mu_i[b] - mu_j[b])^2)
+//   sam:       d = acos(clamp(dot / sqrt(n2_i * n2_j), -1, 1)),
+//              dot = sum_b mu_i[b] * mu_j[b], n2 = sum_b mu[b]^2;
+//              a zero vector gives 0 against a zero vector, pi/2 otherwise.
+// ---------------------------------------------------------------------------
+enum Measure { kBsmse = 0, kEuclid = 1, kSam = 2 };
+
+// fdlibm's e_acos algorithm restated with explicit IEEE operations, so the
+// device and the oracle compute the same bits (SAM ties stay ties).
+__device__ __forceinline__ double rhseg_acos(double x) {
+    const double pi = 3.14159265358979311600e+00, pio2_hi = 1.57079632679489655800e+00,
+                 pio2_lo = 6.12323399573676603587e-17, pS0 = 1.66666666666666657415e-01,
+                 pS1 = -3.25565818622400915405e-01, pS2 = 2.01212532134862925881e-01,
+                 pS3 = -4.00555345006794114027e-02, pS4 = 7.91534994289814532176e-04,
+                 pS5 = 3.47933107596021167570e-05, qS1 = -2.40339491173441421878e+00,
+                 qS2 = 2.02094576023350569471e+00, qS3 = -6.88283971605453293030e-01,
+                 qS4 = 7.70381505559019352791e-02;
+    const int hx = __double2hiint(x);
+    const int ix = hx & 0x7fffffff;
+    if (ix >= 0x3ff00000) {
+        if (((ix - 0x3ff00000) | __double2loint(x)) == 0) return hx > 0 ? 0.0 : __dadd_rn(pi, __dmul_rn(2.0, pio2_lo));
+        return __longlong_as_double(0x7ff8000000000000LL);
+    }
+    auto pq = [&](double z) {
+        const double p = __dmul_rn(
+            z, __dadd_rn(pS0, __dmul_rn(z, __dadd_rn(pS1, __dmul_rn(z, __dadd_rn(pS2, __dmul_rn(z, __dadd_rn(
+                                                        pS3, __dmul_rn(z, __dadd_rn(pS4, __dmul_rn(z, pS5)))))))))));
+        const double q = __dadd_rn(
+            1.0, __dmul_rn(z, __dadd_rn(qS1, __dmul_rn(z, __dadd_rn(qS2, __dmul_rn(z, __dadd_rn(qS3, __dmul_rn(z, qS4))))))));
+        return __ddiv_rn(p, q);
+    };
+    if (ix < 0x3fe00000) {
+        if (ix <= 0x3c600000) return __dadd_rn(pio2_hi, pio2_lo);
+        const double r = pq(__dmul_rn(x, x));
+        return __dsub_rn(pio2_hi, __dsub_rn(x, __dsub_rn(pio2_lo, __dmul_rn(x, r))));
+    } else if (hx < 0) {
+        const double z = __dmul_rn(__dadd_rn(1.0, x), 0.5);
+        const double r = pq(z);
+        const double s = __dsqrt_rn(z);
+        const double w = __dsub_rn(__dmul_rn(r, s), pio2_lo);
+        return __dsub_rn(pi, __dmul_rn(2.0, __dadd_rn(s, w)));
+    } else {
+        const double z = __dmul_rn(__dsub_rn(1.0, x), 0.5);
+        const double s = __dsqrt_rn(z);
+        const double df = __hiloint2double(__double2hiint(s), 0);
+        const double c = __ddiv_rn(__dsub_rn(z, __dmul_rn(df, df)), __dadd_rn(s, df));
+        const double r = pq(z);
+        const double w = __dadd_rn(__dmul_rn(r, s), c);
+        return __dmul_rn(2.0, __dadd_rn(df, w));
+    }
+}
+
+template <int M>
+__device__ __forceinline__ double acc_step(double s, double mi, double mj) {
+    if (M == kSam) return __dadd_rn(s, __dmul_rn(mi, mj));
+    return bsmse_step(s, mi, mj);
+}
+__device__ __forceinline__ double sam_finish(double dot, double n2i, double n2j) {
+    if (n2i == 0.0 || n2j == 0.0) return (n2i == n2j) ? 0.0 : 1.57079632679489655800e+00;
+    double c = __ddiv_rn(dot, __dsqrt_rn(__dmul_rn(n2i, n2j)));
+    c = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+    return rhseg_acos(c);
+}
+// ni/nj: pixel counts, n2i/n2j: squared norms of the means (SAM only).
+template <int M>
+__device__ __forceinline__ double pair_finish(double ni, double nj, double s, double n2i, double n2j) {
+    if (M == kBsmse) return bsmse_finish(ni, nj, s);
+    if (M == kEuclid) return __dsqrt_rn(s);
+    return sam_finish(s, n2i, n2j);
+}
+// n2 of one mean vector: sequential ascending sum of squares (oracle order).
+__device__ __forceinline__ double norm2_seq(const double* mu, size_t stride, int B) {
+    double s = 0.0;
+    for (int k = 0; k < B; ++k) {
+        const double m = mu[(size_t)k * stride];
+        s = __dadd_rn(s, __dmul_rn(m, m));
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
 // Lexicographic keys.
 //   RowBest (d, j): per-row best partner; strict < over ascending j in the
 //     reference (_kernels.py:55, 110) == lexicographic min of (d, j).

@@ -62,6 +62,10 @@ leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int col
             }
             __syncthreads();
         }
+    if (bt.measure == kSam) {  // squared norms of the one-pixel means (sam only)
+        __syncthreads();
+        for (int p = threadIdx.x; p < R0; p += kThreads) bt.nrm2[(size_t)sec * Rp + p] = norm2_seq(mu + p, Rp, B);
+    }
     // grid adjacency (graph.py:20-29 offsets), one writer per row; batch was zeroed
     for (int p = threadIdx.x; p < R0; p += kThreads) {
         const int r = p / e, c = p - r * e;
@@ -192,6 +196,12 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
             }
         }
     }
+    if (pa.measure == kSam) {
+        __syncthreads();
+        const int R = pa.R0[P];  // = live regions over the four children
+        for (int m = threadIdx.x; m < R; m += kThreads)
+            pa.nrm2[(size_t)P * pa.Rp + m] = norm2_seq(pmu + m, pa.Rp, B);
+    }
     // 3. parent pixel assignment
     int* passign = pa.assign + (size_t)P * pa.npx;
     for (int p = threadIdx.x; p < E * E; p += kThreads) {
@@ -253,6 +263,7 @@ graph_init_kernel(SectionBatch bt, const double* __restrict__ counts, const doub
         bt.mu[(size_t)k * Rp + i] = __ddiv_rn(s, n);
         for (int cc = 0; cc < bt.C; ++cc) bt.sums[cc * bt.sums_copy() + (size_t)i * B + k] = s;
     }
+    if (bt.measure == kSam) bt.nrm2[i] = norm2_seq(bt.mu + i, Rp, B);
     for (int64_t p = indptr[i]; p < indptr[i + 1]; ++p) {
         const int j = (int)indices[p];
         for (int cc = 0; cc < bt.C; ++cc) bt.adj[cc * bt.adj_copy() + (size_t)i * W + (j >> 5)] |= 1u << (j & 31);

@@ -406,7 +406,9 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
     host = torch.empty((bands, edge, edge), dtype=torch.float32, pin_memory=True)
     make_cube(name, out=host.numpy())
     cube = host.to(dev)
-    params = RhsegParams(HsegParams(w, t), levels, st)
+    from bench import MEASURE_OF
+
+    params = RhsegParams(HsegParams(w, t, MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
     sh = ShardedRhseg(params, edge, bands, local)
     flush = torch.empty(2 * 126 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     for _ in range(args.warmup):

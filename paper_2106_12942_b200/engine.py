@@ -240,8 +240,16 @@ def _graph_api(graph):
 
 
 def hseg_step(graph, params, strategy=Sequential(), profile: ProfileStats | None = None):
-    """One merge (engine.py:309-342) from device-built per-row tables."""
+    """One merge (engine.py:309-342) from device-built per-row tables. The B3
+    table kernels are sqrt-bsmse only (as _kernels.py is); the extension
+    measures take one step of the device loop instead (same rule, same pick)."""
     resolve_measure(params.measure)
+    if params.measure != "sqrt-bsmse":
+        if graph.live_count <= 1:
+            return None
+        h = hseg_run(graph, HsegParams(params.spectral_weight, graph.live_count - 1, params.measure), strategy,
+                     profile)
+        return h.records[0] if h.records else None
     _, Kind, merge = _graph_api(graph)
     snap = snapshot(graph)
     adjacent = reduce_best(search_table(snap, MergeKind.ADJACENT, strategy, profile))
@@ -293,7 +301,7 @@ def hseg_run(graph, params, strategy=Sequential(), profile: ProfileStats | None 
                     _lib.load().rhseg_hseg_graph(
                         ctx.handle, n, nb, _lib.ptr(snap.counts), _lib.ptr(np.ascontiguousarray(snap.sums)),
                         _lib.ptr(snap.indptr), _lib.ptr(snap.indices), float(params.spectral_weight), target,
-                        int(cluster), _lib.ptr(sa), _lib.ptr(sb), _lib.ptr(sd), _lib.ptr(sk), ctypes.byref(nrec),
+                        int(cluster), MEASURE_CODES[params.measure], _lib.ptr(sa), _lib.ptr(sb), _lib.ptr(sd), _lib.ptr(sk), ctypes.byref(nrec),
                         ctypes.byref(conv),
                     ),
                     "rhseg_hseg_graph",

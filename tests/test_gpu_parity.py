@@ -224,3 +224,57 @@ def test_result_graphs_and_labels_at():
     top = res.labels_at(res.root_hierarchy.initial_region_count - len(res.root_hierarchy.records))
     assert np.array_equal(top.labels, res.labels.labels)
     assert res.labels_at(res.root_initial.live_count).label_count() == res.root_initial.live_count
+
+
+@pytest.mark.parametrize("measure", ["euclidean", "sam"])
+@pytest.mark.parametrize("cluster", [0, 2, 8])
+def test_extension_measures_vs_oracle(measure, cluster, oracle):
+    """euclidean / sam (north-star extensions, no reference implementation):
+    bit-exact against the oracle's restatement, incl. the fdlibm acos on device."""
+    rng = np.random.default_rng(17)
+    cases = []
+    for case in range(8):
+        edge = int(rng.choice([8, 12, 16]))
+        levels = int(rng.integers(1, 4))
+        while edge % (1 << (levels - 1)):
+            levels -= 1
+        bands = int(rng.integers(1, 12))
+        w = float(rng.choice([0.0, 0.21, 1.0]))
+        conn = int(rng.choice([4, 8]))
+        if case % 3 == 0:
+            s = rng.integers(0, 3, size=(bands, edge, edge)).astype(np.float32)
+        else:
+            s = rng.normal(40, 25, size=(bands, edge, edge)).astype(np.float32)
+        t = int(rng.integers(1, 8))
+        cases.append((s, levels, w, t, int(rng.integers(t, t + 10)), conn))
+    img, _ = rh.gen_synthetic(32, 12, 4, 6, 3.0, 32)
+    cases.append((img.samples, 2, 0.21, 4, 9, 8))
+    oracle.set_measure(measure)
+    try:
+        for k, (s, levels, w, t, st, conn) in enumerate(cases):
+            bands, edge, _ = s.shape
+            img = rh.HyperImage(edge, edge, bands, s)
+            res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(w, t, measure), levels, st),
+                               executor=rh.B200Executor(connectivity=conn, cluster=cluster))
+            ref = oracle.rhseg_run(s, levels, w, t, st, connectivity=conn)
+            assert_log_equal(_flat(res), ref, f"{measure} case {k}")
+            assert np.array_equal(res.labels.labels, ref["labels"])
+            assert res.converged_early == ref["converged_early"]
+    finally:
+        oracle.set_measure("sqrt-bsmse")
+
+
+@pytest.mark.parametrize("measure", ["euclidean", "sam"])
+def test_extension_measures_hseg_run_and_step(measure, oracle):
+    img, _ = rh.gen_synthetic(16, 6, 4, 6, 3.0, 5)
+    g = rh.init_region_graph(img, 8)
+    h = rh.hseg_run(g, rh.HsegParams(0.5, 3, measure))
+    fn = rh.MEASURES[measure]
+    replay = rh.init_region_graph(img, 8)
+    for rec in h.records:
+        assert rec.dissimilarity == fn(replay.region(rec.survivor_id), replay.region(rec.absorbed_id))
+        rh.merge_regions(replay, rec.survivor_id, rec.absorbed_id, rec.dissimilarity, rec.kind)
+    g2 = rh.init_region_graph(img, 8)
+    first = rh.hseg_step(g2, rh.HsegParams(0.5, 3, measure))
+    assert (first.survivor_id, first.absorbed_id, first.dissimilarity) == (
+        h.records[0].survivor_id, h.records[0].absorbed_id, h.records[0].dissimilarity)

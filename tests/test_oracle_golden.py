@@ -86,3 +86,35 @@ def test_oracle_synthetic_rhseg(name):
     _check_log(res, z)
     assert np.array_equal(res["labels"], z["labels"])
     assert np.array_equal(res["assignment"].ravel(), z["assignment"])
+
+
+def test_extension_measures_known_answers(oracle):
+    """euclidean / sam (north-star extensions; no reference oracle): hand-checked
+    values through the oracle's hseg on tiny graphs, and the fdlibm acos
+    restatement agreeing with libm to 1 ulp and with the Python scalar bitwise."""
+    import math
+
+    from paper_2106_12942_b200.dissim import acos_fdlibm, euclidean_scalar, sam_scalar
+
+    assert euclidean_scalar(1, 1, [0.0, 0.0], [3.0, 4.0]) == 5.0
+    assert sam_scalar(1, 1, [1.0, 0.0], [0.0, 2.0]) == acos_fdlibm(0.0)
+    assert abs(sam_scalar(1, 1, [1.0, 0.0], [0.0, 2.0]) - math.pi / 2) < 1e-15
+    assert sam_scalar(2, 3, [2.0, 4.0], [3.0, 6.0]) == 0.0
+    assert sam_scalar(1, 1, [0.0, 0.0], [0.0, 0.0]) == 0.0
+    rng = np.random.default_rng(3)
+    for x in np.concatenate([rng.uniform(-1, 1, 20000), [1.0, -1.0, 0.0, 0.5, -0.5, 1 - 2 ** -53]]):
+        a = oracle.acos(float(x))
+        assert a == acos_fdlibm(float(x))
+        assert abs(a - math.acos(x)) <= math.ulp(math.acos(x))
+    # two regions, one merge: the recorded dissimilarity is the scalar formula
+    for name, fn in (("euclidean", euclidean_scalar), ("sam", sam_scalar), ("sqrt-bsmse", None)):
+        oracle.set_measure(name)
+        try:
+            r = oracle.hseg_graph([1, 1], [[1.0, 2.0], [4.0, 6.0]], [[0, 1], [1, 0]], 0.21, 1)
+        finally:
+            oracle.set_measure("sqrt-bsmse")
+        d = r["records"][2][0]
+        if fn is not None:
+            assert d == fn(1, 1, [1.0, 2.0], [4.0, 6.0]), name
+        else:
+            assert d == math.sqrt(0.5 * 25.0)
