@@ -861,6 +861,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         mark(3);
         // (E) rescan rows whose cached partner was a or b
         const int ni = ninv;
+        if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
         for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3);
         __syncthreads();
         mark(4);
@@ -874,7 +875,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (tid == 0) {
             bt.nlog[sec] = step;
             if (bt.prof)
-                for (int q = 0; q < 5; ++q) atomicAdd(bt.prof + q, pc[q]);
+                for (int q = 0; q < 6; ++q) atomicAdd(bt.prof + q, pc[q]);
             bt.conv[sec] = conv;
             if (bt.pairs) bt.pairs[sec] = pairs;
         }
