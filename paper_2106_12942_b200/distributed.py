@@ -255,6 +255,26 @@ class ShardedRhseg:
         self.runner = RankRunner(ex.c_params(params), edge, bands, params.levels, device)
         self.edge, self.bands = edge, bands
         self._bufs = {}
+        # NCCL moves device buffers directly; gloo (CPU tests, several ranks on one
+        # device) stages them through host memory
+        self.host_comm = dist.get_backend() != "nccl"
+
+    def _all_gather(self, out, t):
+        if not self.host_comm:
+            return self.dist.all_gather(out, t)
+        tmp = [o.cpu() for o in out]
+        self.dist.all_gather(tmp, t.cpu())
+        for o, x in zip(out, tmp):
+            o.copy_(x)
+
+    def _gather(self, t, out):
+        if not self.host_comm:
+            return self.dist.gather(t, out, dst=0)
+        tmp = [o.cpu() for o in out] if out is not None else None
+        self.dist.gather(t.cpu(), tmp, dst=0)
+        if out is not None:
+            for o, x in zip(out, tmp):
+                o.copy_(x)
 
     def _buf(self, name, n, dtype):
         t = self._bufs.get(name)
@@ -290,7 +310,7 @@ class ShardedRhseg:
             meta[1:1 + nsec] = torch.from_numpy(R0).to(self.dev)
             meta[1 + maxn:1 + maxn + nsec] = torch.from_numpy(nlog).to(self.dev)
         metas = [torch.empty_like(meta) for _ in range(self.world)]
-        dist.all_gather(metas, meta)
+        self._all_gather(metas, meta)
         allm = torch.stack(metas).cpu().numpy()
         rpc = int(allm[:, 0].max())
         pbytes = self.runner.pack_bytes(rpc, se)
@@ -299,7 +319,8 @@ class ShardedRhseg:
             self.runner.export(rpc, pack.data_ptr(), stream)
         # the one data-path collective: section states -> rank 0
         gl = [self._buf(f"g{r}", maxn * pbytes, torch.uint8) for r in range(self.world)] if self.rank == 0 else None
-        dist.gather(pack, gl, dst=0)
+        self.torch.cuda.synchronize(self.dev)  # the export ran on the library's stream
+        self._gather(pack, gl)
         logs = self._gather_logs() if gather_logs else None
         if self.rank == 0:
             allp = self._buf("allpack", S * pbytes, torch.uint8)
@@ -326,7 +347,7 @@ class ShardedRhseg:
             secs, n = np.zeros((0, 5), np.int64), 0
         sizes = torch.tensor([n, secs.shape[0]], dtype=torch.int64, device=self.dev)
         alls = [torch.empty_like(sizes) for _ in range(self.world)]
-        dist.all_gather(alls, sizes)
+        self._all_gather(alls, sizes)
         alls = torch.stack(alls).cpu().numpy()
         nmax, smax = int(alls[:, 0].max()), int(alls[:, 1].max())
         a = self._buf("la", nmax, torch.int32)
@@ -341,7 +362,7 @@ class ShardedRhseg:
         out = []
         for name, t in (("a", a), ("b", b), ("d", d), ("k", k), ("s", st)):
             g = [torch.empty_like(t) for _ in range(self.world)] if self.rank == 0 else None
-            dist.gather(t.contiguous(), g, dst=0)
+            self._gather(t.contiguous(), g)
             out.append(g)
         if self.rank != 0:
             return None

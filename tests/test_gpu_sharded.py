@@ -37,3 +37,27 @@ def test_sharded_equals_single(world, w, oracle):
     ref = oracle.rhseg_run(img.samples, 4, w, 6, 12)
     assert np.array_equal(fb[2].view(np.uint64), ref["log_dissim"].view(np.uint64))
     assert np.array_equal(shard.labels.labels, ref["labels"])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_torchrun_sharded_step(world, tmp_path):
+    """The torch.distributed path itself (plan, export, gather, rank-0 upper
+    levels, log gather + canonical reassembly) under torchrun; gloo stands in
+    for NCCL because every rank shares the one GPU of the test box."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "res.json"
+    worker = os.path.join(os.path.dirname(__file__), "sharded_worker.py")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", worker, str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert res["ok"] and res["records"] > 0 and res["world"] == world
