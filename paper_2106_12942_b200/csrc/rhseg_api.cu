@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -134,6 +135,10 @@ struct rhseg_ctx {
     float phase_ms[4] = {0, 0, 0, 0};
     bool phases_valid = false;
     long long launches = 0;  // kernels launched by the last run (+ result copies since)
+    // Device buffers cached across runs (grown, never shrunk, freed with the ctx):
+    // repeated runs of one shape allocate nothing, so no run waits on the driver.
+    std::map<int, std::pair<void*, size_t>> bufs;
+    size_t dmat_budget = 0;  // bytes the D matrix may use (measured once per ctx)
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -163,20 +168,28 @@ struct PhaseTimer {
     }
 };
 
-static void free_level(Level& lv, cudaStream_t st) {
-    if (lv.work) cudaFreeAsync(lv.work, st);
-    if (lv.keep) cudaFreeAsync(lv.keep, st);
-    lv.work = lv.keep = nullptr;
+enum BufKey { kBufSnap = 1, kBufDmat = 2, kBufLog = 3, kBufCube = 4, kBufLogOff = 5, kBufLevel = 100 };
+
+// Cached device buffer `key` with at least `bytes` (contents undefined).
+static int get_buf(rhseg_ctx* c, int key, size_t bytes, void** out) {
+    auto& b = c->bufs[key];
+    if (b.second < bytes) {
+        if (b.first) CK(cudaFree(b.first));
+        b.first = nullptr;
+        b.second = 0;
+        CK(cudaMalloc(&b.first, std::max<size_t>(bytes, 256)));
+        b.second = std::max<size_t>(bytes, 256);
+    }
+    *out = b.first;
+    return RHSEG_OK;
 }
-static void free_work(Level& lv, cudaStream_t st) {
-    if (lv.work) cudaFreeAsync(lv.work, st);
-    lv.work = nullptr;
-}
+
+static void free_level(Level& lv, cudaStream_t) { lv.work = lv.keep = nullptr; }  // buffers stay cached
+static void free_work(Level& lv, cudaStream_t) { lv.work = nullptr; }
 
 static void reset_ctx(rhseg_ctx* c, cudaStream_t st) {
     for (auto& lv : c->levels) free_level(lv, st);
     c->levels.clear();
-    if (c->snap) cudaFreeAsync(c->snap, st);
     c->snap = nullptr;
     c->have = false;
     c->top = 1;
@@ -196,7 +209,7 @@ static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced) {
 }
 
 // Allocate and zero one level's device state. R0h/tgth must be filled.
-static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, int forced_C) {
+static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, int forced_C, int slot) {
     lv.R0max = 0;
     for (int r : lv.R0h) lv.R0max = std::max(lv.R0max, r);
     if (lv.R0max > 16384)
@@ -225,7 +238,10 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
                  oLb = take(ns * Rp * 4), oLd = take(ns * Rp * 8), oLk = take(ns * Rp), oN = take(ns * 4),
                  oCv = take(ns * 4), oPr = take(ns * 8), oN2 = take(lv.measure == 2 ? ns * Rp * 8 : 0);
     const size_t keep_bytes = o;
-    CK(cudaMallocAsync(&lv.keep, keep_bytes, st));
+    {
+        int rc = get_buf(c, kBufLevel + 2 * slot, keep_bytes, &lv.keep);
+        if (rc) return rc;
+    }
     CK(cudaMemsetAsync(lv.keep, 0, keep_bytes, st));
     o = 0;
     const size_t oAdj = take(ns * C * Rp * W * 4);
@@ -233,7 +249,10 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec ? ns * B * Rp * 8 : 0),
                  oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
-    CK(cudaMallocAsync(&lv.work, work_bytes, st));
+    {
+        int rc = get_buf(c, kBufLevel + 2 * slot + 1, work_bytes, &lv.work);
+        if (rc) return rc;
+    }
     CK(cudaMemsetAsync(lv.work, 0, lv.work_zero, st));
     char* K = static_cast<char*>(lv.keep);
     char* Wk = static_cast<char*>(lv.work);
@@ -304,18 +323,21 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     lv.sb.prof = prof;
     const double t_enter = prof ? now_ms() : 0.0;
     const size_t dsec = (size_t)lv.Rp * lv.Rp * 8;
-    size_t freeb = 0, totalb = 0;
     RHSEG_TRACE("run_level %d: enter", lv.level);
-    CK(cudaMemGetInfo(&freeb, &totalb));
-    RHSEG_TRACE("run_level %d: meminfo", lv.level);
-    size_t budget = (size_t)(0.6 * (double)(freeb + c->dmat_bytes));
-    size_t chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, budget / dsec));
+    size_t chunk = (size_t)lv.nsec;
     if (c->dmat_bytes < chunk * dsec) {
-        if (c->dmat) CK(cudaFreeAsync(c->dmat, st));
-        c->dmat = nullptr;
-        c->dmat_bytes = 0;
-        CK(cudaMallocAsync(&c->dmat, chunk * dsec, st));
-        c->dmat_bytes = chunk * dsec;
+        // D for every section of the level at once if it fits 60% of what is free
+        // (queried only when the cached D is too small)
+        size_t freeb = 0, totalb = 0;
+        CK(cudaMemGetInfo(&freeb, &totalb));
+        const size_t budget = (size_t)(0.6 * (double)(freeb + c->dmat_bytes));
+        chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, budget / dsec));
+        if (c->dmat_bytes < chunk * dsec) {
+            int rc = get_buf(c, kBufDmat, chunk * dsec, &c->dmat);
+            if (rc) return rc;
+            c->dmat_bytes = chunk * dsec;
+        }
+        chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, c->dmat_bytes / dsec));
     }
     lv.sb.D = static_cast<double*>(c->dmat);
     for (size_t s0 = 0; s0 < (size_t)lv.nsec; s0 += chunk) {
@@ -381,7 +403,10 @@ static int snapshot_root(rhseg_ctx* c, Level& lv, cudaStream_t st) {
     };
     const size_t oc = take(Rp * 4), os = take(Rp * B * 8), oa = take(Rp * W * 4), oas = take(npx * 4),
                  olab = take(npx * 4), of = take(Rp * 4), orank = take(Rp * 4);
-    CK(cudaMallocAsync(&c->snap, o, st));
+    {
+        int rc = get_buf(c, kBufSnap, o, &c->snap);
+        if (rc) return rc;
+    }
     char* S = static_cast<char*>(c->snap);
     c->init_count = reinterpret_cast<uint32_t*>(S + oc);
     c->init_sums = reinterpret_cast<double*>(S + os);
@@ -482,7 +507,7 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
         }
         pa.tgth.assign(pa.nsec, level == 1 ? p->target_regions : sect);
         RHSEG_TRACE("level %d: alloc", level);
-        int rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster);
+        int rc = alloc_level(c, pa, p->spectral_weight, st, p->cluster, (int)c->levels.size());
         RHSEG_TRACE("level %d: alloc done", level);
         if (rc) return rc;
         {
@@ -565,7 +590,7 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         lv.R0h.assign(lv.nsec, e * e);
         lv.tgth.assign(lv.nsec, L == 1 ? p->target_regions : sect);
         RHSEG_TRACE("leaves: alloc");
-        rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster);
+        rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster, 0);
         RHSEG_TRACE("leaves: alloc done");
         if (rc) return rc;
         {
@@ -644,8 +669,10 @@ int rhseg_ctx_destroy(rhseg_ctx* c) {
     if (!c) return RHSEG_OK;
     cudaSetDevice(c->device);
     reset_ctx(c, c->stream);
-    if (c->dmat) cudaFreeAsync(c->dmat, c->stream);
     cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->bufs)
+        if (kv.second.first) cudaFree(kv.second.first);
+    c->bufs.clear();
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -742,7 +769,7 @@ int rhseg_run_upper(rhseg_ctx* c, const void* d_pack, int32_t top_level, int32_t
     int rpmax = 0;
     for (int r : lv.R0h) rpmax = std::max(rpmax, r);
     if (rpmax > rp) return fail(RHSEG_E_INVALID, "a section's R0 exceeds rp");
-    rc = alloc_level(c, lv, p->spectral_weight, st, 1);
+    rc = alloc_level(c, lv, p->spectral_weight, st, 1, 0);
     if (rc) return rc;
     const PackLayout P = pack_layout(rp, bands, lv.edge);
     const size_t B = bands, W = lv.W, Wi = rp / 32, npx = (size_t)lv.edge * lv.edge;
@@ -824,7 +851,12 @@ static int compact_log(rhseg_ctx* c, int32_t* da, int32_t* db, double* dd, uint8
     }
     if (base == 0) return RHSEG_OK;
     long long* doff = nullptr;
-    CK(cudaMallocAsync(&doff, 8 * off.size(), st));
+    {
+        void* p = nullptr;
+        int rc = get_buf(c, kBufLogOff, 8 * off.size(), &p);
+        if (rc) return rc;
+        doff = static_cast<long long*>(p);
+    }
     CK(cudaMemcpyAsync(doff, off.data(), 8 * off.size(), cudaMemcpyHostToDevice, st));
     for (size_t L = 0; L < c->levels.size(); ++L) {
         Level& lv = c->levels[L];
@@ -834,7 +866,6 @@ static int compact_log(rhseg_ctx* c, int32_t* da, int32_t* db, double* dd, uint8
         CK(cudaGetLastError());
         c->launches += 1;
     }
-    CK(cudaFreeAsync(doff, st));
     CK(cudaStreamSynchronize(st));  // `off` must outlive the async H2D copy
     return RHSEG_OK;
 }
@@ -843,7 +874,12 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
     const int64_t n = c->info.n_records;
     if (n == 0) return RHSEG_OK;
     int* da = nullptr;
-    CK(cudaMallocAsync(&da, (size_t)n * 17 + 1024, st));
+    {
+        void* p = nullptr;
+        int rc = get_buf(c, kBufLog, (size_t)n * 17 + 1024, &p);
+        if (rc) return rc;
+        da = static_cast<int*>(p);
+    }
     int* db = da + n;
     double* dd = reinterpret_cast<double*>(db + n);  // 2n ints: 8-byte aligned
     uint8_t* dk = reinterpret_cast<uint8_t*>(dd + n);
@@ -853,7 +889,6 @@ static int copy_log(rhseg_ctx* c, int32_t* sa, int32_t* sb, double* sd, uint8_t*
     if (sb) CK(cudaMemcpyAsync(sb, db, 4 * (size_t)n, cudaMemcpyDeviceToHost, st));
     if (sd) CK(cudaMemcpyAsync(sd, dd, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
     if (sk) CK(cudaMemcpyAsync(sk, dk, (size_t)n, cudaMemcpyDeviceToHost, st));
-    CK(cudaFreeAsync(da, st));
     CK(cudaStreamSynchronize(st));
     return RHSEG_OK;
 }
@@ -919,10 +954,14 @@ int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t b
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
     const size_t bytes = (size_t)edge * edge * bands * sizeof(float);
     float* d = nullptr;
-    CK(cudaMallocAsync(&d, bytes, st));
+    {
+        void* p = nullptr;
+        rc = get_buf(c, kBufCube, bytes, &p);
+        if (rc) return rc;
+        d = static_cast<float*>(p);
+    }
     CK(cudaMemcpyAsync(d, h_samples, bytes, cudaMemcpyHostToDevice, st));
     rc = run_device_impl(c, d, edge, bands, p, 1, 0, 0, 1, 1, st);
-    cudaFreeAsync(d, st);
     if (rc) return rc;
     rc = copy_log(c, log_survivor, log_absorbed, log_dissim, log_kind, st);
     if (rc) return rc;
@@ -964,7 +1003,7 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
     lv.measure = measure;
     lv.R0h.assign(1, (int)n);
     lv.tgth.assign(1, (int)std::min<int64_t>(target, INT32_MAX));
-    int rc = alloc_level(c, lv, weight, st, cluster);
+    int rc = alloc_level(c, lv, weight, st, cluster, 0);
     if (rc) return rc;
     const int64_t nnz = indptr[n];
     void* tmp = nullptr;
