@@ -257,17 +257,11 @@ __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool ne
         if (isadj) rb_offer(pA, d, jq);
         else rb_offer(pN, d, jq);
     }
+    // rows whose cached partner was a or b were rescanned (a and b excluded)
+    // before this pass, so every row just takes the offer of (d(j, a), a)
     const int r = jq - lo;
-    int mask = 0;
-    const int ja = bAj[r];
-    if (ja == a || ja == b) mask |= 1;
-    else if (isadj) cache_offer(bAd[r], bAj[r], d, a);
-    if (SPEC) {
-        const int jn = bNj[r];
-        if (jn == a || jn == b) mask |= 2;
-        else if (!isadj) cache_offer(bNd[r], bNj[r], d, a);
-    }
-    if (mask) inv[atomicAdd(ninv, 1)] = (jq << 2) | mask;
+    if (isadj) cache_offer(bAd[r], bAj[r], d, a);
+    else if (SPEC) cache_offer(bNd[r], bNj[r], d, a);
 }
 
 // w = 0 row-a pass: only a's neighbours need a dissimilarity (the spectral stage
@@ -372,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // partner was merged away. Adjacent-only rescans walk the adjacency bitset;
     // non-adjacent ones stream the D row with 8 loads in flight per lane.
     StreamState ss{};
-    auto rescan = [&](int i, int mask) {
+    auto rescan = [&](int i, int mask, int ex) {  // ex: column skipped (-1 = none)
         RowBest ba = rb_none(), bn = rb_none();
         if (cnt[i] != 0u) {
             const uint32_t* arow = adj + (size_t)i * W;
@@ -384,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     while (bits) {
                         const int j = (w << 5) + __ffs(bits) - 1;
                         bits &= bits - 1;
-                        if (j < R0 && cnt[j] != 0u) rb_offer(ba, __ldcg(drow + j), j);
+                        if (j < R0 && j != ex && cnt[j] != 0u) rb_offer(ba, __ldcg(drow + j), j);
                     }
                 }
             } else if (!CLUSTER) {
@@ -404,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int j = jv[u];
-                        if (j >= 0 && j != i && cnt[j] != 0u) {
+                        if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
                             if ((arow[j >> 5] >> (j & 31)) & 1u) {
                                 if (mask & 1) rb_offer(ba, dv[u], j);
                             } else {
@@ -427,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int j = j0 + 32 * u + lane;
-                        if (j < R0 && j != i && cnt[j] != 0u) {
+                        if (j < R0 && j != i && j != ex && cnt[j] != 0u) {
                             if ((wv[u] >> lane) & 1u) {
                                 if (mask & 1) rb_offer(ba, dv[u], j);
                             } else {
@@ -561,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         rpart[1] = rb_none();
     }
     __syncthreads();
-    for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1);
+    for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1, -1);
     long long E = 0;
     if (SPEC && rank == 0) {
         unsigned long long e = 0;
@@ -708,6 +702,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (SPEC && dE) atomicAdd(&sdE, dE);
         }
         if (tid == 0) {
+            cnt[a] = (uint32_t)nn;
+            cnt[b] = 0u;
             if (own_a) {
                 bAd[a - lo] = kInf; bAj[a - lo] = -1;
                 bNd[a - lo] = kInf; bNj[a - lo] = -1;
@@ -727,8 +723,28 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
         __syncthreads();
         if (SPEC) E += sdE;
-
         mark(2);
+
+        // (C2) rows whose cached partner was a or b: rescan them from D now,
+        // skipping a (its entries are refreshed by the row-a pass, which then
+        // offers (d(i, a), a) to every row) and b (dead). Their D loads overlap the
+        // row-a stream already in flight.
+        for (int i = lo + tid; i < hi; i += kThreads) {
+            if (cnt[i] == 0u || i == a) continue;
+            const int r = i - lo;
+            int mask = 0;
+            if (bAj[r] == a || bAj[r] == b) mask |= 1;
+            if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
+            if (mask) inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
+        }
+        __syncthreads();
+        {
+            const int ni = ninv;
+            if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
+            for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
+        }
+        __syncthreads();
+        mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
         double n2a = 0.0;
@@ -846,8 +862,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             rpart[0] = pA;
             rpart[1] = pN;
             if (SPEC) sdE = 0;
-            cnt[a] = (uint32_t)nn;
-            cnt[b] = 0u;
             if (SPEC && b >= lo && b < hi) {  // b's column becomes a hole of the stream
                 col[slot_of[b - lo]] = -1;
                 slot_of[b - lo] = -1;
@@ -859,12 +873,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (RHSEG_EARLY_STREAM && SPEC && R0 - (step + 1) > target) begin_stream();
 
         mark(3);
-        // (E) rescan rows whose cached partner was a or b
-        const int ni = ninv;
-        if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
-        for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3);
-        __syncthreads();
-        mark(4);
         a_prev = a;
         ++step;
         if (!RHSEG_EARLY_STREAM && SPEC && R0 - step > target) begin_stream();
