@@ -373,6 +373,17 @@ def measured_peaks():
         return {}
 
 
+def ncu_traffic(name, kernel):
+    """DRAM bytes (read + write) of one leaf-level launch from the committed ncu
+    capture (profiles/traffic.json), or None when this workload was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f).get(name, {}).get(kernel)
+    except (OSError, ValueError):
+        return None
+    return None if not t else t["dram_read_bytes"] + t["dram_write_bytes"]
+
+
 def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
     """Dominant kernel = the longer of the merge loop (phase 2) and the
     all-pairs D init (phase 1). Algorithmic work per DESIGN.md §4:
@@ -398,7 +409,8 @@ def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
         algo = nleaf * per_sec
         achieved = algo / (loop_ms * 1e-3) / 1e9
         return {"kernel": "hseg_loop_kernel (persistent per-section merge loop)", "bound": "hbm",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": ncu_traffic(name, "hseg_loop_kernel"),
                 "algorithmic_bytes": algo, "kernel_ms": loop_ms,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
     fp64 = ctypes.c_double(0.0)
@@ -412,7 +424,7 @@ def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
     peak = fp64.value / 1e12
     return {"kernel": "dinit_dense_kernel (all-pairs fp64 dissimilarity)", "bound": "fp64",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-            "traffic": None, "kernel_ms": dinit_ms,
+            "traffic": ncu_traffic(name, "dinit_dense_kernel"), "kernel_ms": dinit_ms,
             "peak_source": "measured live by rhseg_fp64_peak (DSUB+DMUL+DADD issue rate); "
                            "MEASURED_PEAKS.json has no fp64 figure"}
 
