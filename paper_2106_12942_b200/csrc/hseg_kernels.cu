@@ -200,15 +200,19 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #endif
 constexpr int kStages = RHSEG_STAGES;
 constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
+// SAM keeps the two best partners per row (TOP2 below) and pays for those
+// arrays with a smaller stream ring, so two CTAs still fit one SM.
+constexpr int kStageBytesTop2 = 20 * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
-    size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, ring, total;
+    size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+        bAj2, bNj2, cx, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
-__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec) {
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2) {
     const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
     size_t o = 0;
@@ -228,26 +232,103 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.cnt = o;   o = align16(o + (size_t)Rp * 4);
     L.col = o;   o = align16(o + (spec ? Rs * 4 : 0));
     L.slot_of = o; o = align16(o + (spec ? Rs * 4 : 0));
+    L.bAd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
+    L.bNd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
+    L.bAj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
+    L.bNj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
+    L.cx = o;    o = align16(o + (top2 ? Rs : 0));
     o = (o + 127) & ~size_t(127);
-    L.ring = o;  o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * kStageBytes + kThreads * 8 : 0;  // + overrun pad
+    L.ring = o;
+    o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * (top2 ? kStageBytesTop2 : kStageBytes) + kThreads * 8 : 0;
     L.total = o;
     return L;
 }
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec) { return loop_smem_layout(Rp, C, B, spec).total; }
+__host__ __device__ inline bool use_top2(bool spec, int C, int measure) { return spec && C == 1 && measure == kSam; }
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure) {
+    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure)).total;
+}
 int hseg_loop_max_rows() { return kMaxSlots; }
 
 __device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j) {
     if (d < kInf && (d < cd || (d == cd && j < cj))) { cd = d; cj = j; }
 }
 
+// ---- TOP2 (SAM): the two smallest (d, j) candidates of a row and stage -------
+// A row's list holds its m <= 2 lexicographically smallest candidates; the
+// "complete" bit says the list holds every candidate. A merge (a, b) removes a
+// and b from every list and offers (d(i, a), a); only a list left empty and
+// incomplete needs a rescan from D. Equivalent to the reference's per-row best
+// (its head) at every step, with far fewer rescans when many rows share a best
+// partner (SAM: a merged region becomes the nearest angle of most rows).
+struct Top2 {
+    double d0;
+    int j0;
+    double d1;
+    int j1;
+    int n;  // candidates seen, capped at 3
+};
+__device__ __forceinline__ Top2 t2_none() { return Top2{kInf, kNoJ, kInf, kNoJ, 0}; }
+__device__ __forceinline__ void t2_put(Top2& t, double d, int j) {
+    if (!(d < kInf)) return;
+    if (d < t.d0 || (d == t.d0 && j < t.j0)) {
+        t.d1 = t.d0; t.j1 = t.j0; t.d0 = d; t.j0 = j;
+    } else if (d < t.d1 || (d == t.d1 && j < t.j1)) {
+        t.d1 = d; t.j1 = j;
+    }
+}
+__device__ __forceinline__ void t2_offer(Top2& t, double d, int j) {
+    if (!(d < kInf)) return;
+    t.n = min(t.n + 1, 3);
+    t2_put(t, d, j);
+}
+__device__ __forceinline__ Top2 warp_top2(Top2 t) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d0 = __shfl_xor_sync(0xffffffffu, t.d0, o), d1 = __shfl_xor_sync(0xffffffffu, t.d1, o);
+        const int j0 = __shfl_xor_sync(0xffffffffu, t.j0, o), j1 = __shfl_xor_sync(0xffffffffu, t.j1, o);
+        const int n = __shfl_xor_sync(0xffffffffu, t.n, o);
+        t2_put(t, d0, j0);
+        t2_put(t, d1, j1);
+        t.n = min(t.n + n, 3);
+    }
+    return t;
+}
+__device__ __forceinline__ void l2_remove(double& d0, int& j0, double& d1, int& j1, int x) {
+    if (j1 == x) { d1 = kInf; j1 = -1; }
+    if (j0 == x) { d0 = d1; j0 = j1; d1 = kInf; j1 = -1; }
+}
+__device__ __forceinline__ void l2_offer(double& d0, int& j0, double& d1, int& j1, uint8_t& cbits, uint8_t bit,
+                                         double d, int j) {
+    if (!(d < kInf)) return;
+    const bool complete = (cbits & bit) != 0;
+    if (j0 < 0) {
+        if (complete) { d0 = d; j0 = j; }
+        return;
+    }
+    const bool lt0 = d < d0 || (d == d0 && j < j0);
+    if (j1 < 0) {
+        if (lt0) { d1 = d0; j1 = j0; d0 = d; j0 = j; }
+        else if (complete) { d1 = d; j1 = j; }
+        return;
+    }
+    if (lt0) { d1 = d0; j1 = j0; d0 = d; j0 = j; }
+    else if (d < d1 || (d == d1 && j < j1)) { d1 = d; j1 = j; }
+    cbits &= (uint8_t)~bit;  // a third candidate exists and is not stored
+}
+struct Top2Lists {
+    double *bAd2, *bNd2;
+    int *bAj2, *bNj2;
+    uint8_t* cx;
+};
+
 // Epilogue for one column j of the row-a pass: D row/column update, offer
 // (d, a) to row j's caches, mark rows whose cached partner died.
-template <bool SPEC, int M>
+template <bool SPEC, int M, bool TOP2 = false>
 __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool need, double s, double nn, int a,
                                          int b, int lo, int Rp, const uint32_t* cnt, double n2a,
                                          const double* __restrict__ n2, double* __restrict__ D,
                                          double* bAd, int* bAj, double* bNd, int* bNj, RowBest& pA, RowBest& pN,
-                                         int* inv, int* ninv) {
+                                         int* inv, int* ninv, Top2Lists t2 = Top2Lists{}) {
     if (!valid) return;
     double d = kInf;
     if (need) {
@@ -260,6 +341,11 @@ __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool ne
     // rows whose cached partner was a or b were rescanned (a and b excluded)
     // before this pass, so every row just takes the offer of (d(j, a), a)
     const int r = jq - lo;
+    if (TOP2) {
+        if (isadj) l2_offer(bAd[r], bAj[r], t2.bAd2[r], t2.bAj2[r], t2.cx[r], 1, d, a);
+        else l2_offer(bNd[r], bNj[r], t2.bNd2[r], t2.bNj2[r], t2.cx[r], 2, d, a);
+        return;
+    }
     if (isadj) cache_offer(bAd[r], bAj[r], d, a);
     else if (SPEC) cache_offer(bNd[r], bNj[r], d, a);
 }
@@ -330,7 +416,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     const int Rs = own_rows(R0, C);
     const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
 
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC);
+    constexpr bool TOP2 = SPEC && !CLUSTER && M == kSam;
+    constexpr int SB = TOP2 ? kStageBytesTop2 : kStageBytes;
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -352,6 +440,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
     int* col = reinterpret_cast<int*>(smem + L.col);
     int* slot_of = reinterpret_cast<int*>(smem + L.slot_of);
+    // TOP2: second-best partner per row and stage + "list holds every candidate" bits
+    double* bAd2 = reinterpret_cast<double*>(smem + L.bAd2);
+    double* bNd2 = reinterpret_cast<double*>(smem + L.bNd2);
+    int* bAj2 = reinterpret_cast<int*>(smem + L.bAj2);
+    int* bNj2 = reinterpret_cast<int*>(smem + L.bNj2);
+    uint8_t* cx = reinterpret_cast<uint8_t*>(smem + L.cx);
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
     double* const mu0 = bt.mu + sec * bt.mu_stride();
@@ -441,6 +535,56 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
     };
 
+    // TOP2 rescan: the two best candidates per masked stage + the complete bit,
+    // over the compacted live-column list (one CTA owns every column).
+    auto rescan2 = [&](int i, int mask, int ex) {
+        Top2 ta = t2_none(), tn = t2_none();
+        if (cnt[i] != 0u) {
+            const uint32_t* arow = adj + (size_t)i * W;
+            const double* drow = D + (size_t)i * Rp;
+            constexpr int U = 16;
+            for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                double dv[U];
+                int jv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int sl = s0 + 32 * u + lane;
+                    const int j = sl < ss.S ? col[sl] : -1;
+                    jv[u] = j;
+                    dv[u] = j >= 0 ? __ldcs(drow + j) : kInf;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = jv[u];
+                    if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                        if ((arow[j >> 5] >> (j & 31)) & 1u) {
+                            if (mask & 1) t2_offer(ta, dv[u], j);
+                        } else if (mask & 2) {
+                            t2_offer(tn, dv[u], j);
+                        }
+                    }
+                }
+            }
+        }
+        ta = warp_top2(ta);
+        tn = warp_top2(tn);
+        if (lane == 0) {
+            const int r = i - lo;
+            uint8_t c = cx[r];
+            if (mask & 1) {
+                bAd[r] = ta.d0; bAj[r] = ta.j0 == kNoJ ? -1 : ta.j0;
+                bAd2[r] = ta.d1; bAj2[r] = ta.j1 == kNoJ ? -1 : ta.j1;
+                c = ta.n <= 2 ? (c | 1) : (c & ~1);
+            }
+            if (mask & 2) {
+                bNd[r] = tn.d0; bNj[r] = tn.j0 == kNoJ ? -1 : tn.j0;
+                bNd2[r] = tn.d1; bNj2[r] = tn.j1 == kNoJ ? -1 : tn.j1;
+                c = tn.n <= 2 ? (c | 2) : (c & ~2);
+            }
+            cx[r] = c;
+        }
+    };
+
     // ---- streaming ring (SPEC) ----
     // Stage `i` of the current step into ring slot abs_stage % kStages. Called by
     // all lanes of warp 0: lane 0 arms the full barrier, the lanes issue one bulk
@@ -458,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
         }
         __syncwarp();
-        char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * kStageBytes;
+        char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * SB;
         const double* src = (ss.cur ? mu1 : mu0) + lo;
         for (int kk = lane; kk < kb; kk += 32)
             bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
@@ -520,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     auto begin_stream = [&]() {
         if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
         ss.S2 = (ss.S + 1) & ~1;
-        ss.KB = ss.S2 > 0 ? max(1, min(B, kStageBytes / (ss.S2 * 8))) : B;
+        ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * 8))) : B;
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
         ss.pf = 0;
@@ -555,7 +699,13 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         rpart[1] = rb_none();
     }
     __syncthreads();
-    for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1, -1);
+    if (TOP2) {
+        for (int r = tid; r < hi - lo; r += kThreads) cx[r] = 0;
+        __syncthreads();
+        for (int i = lo + warp; i < hi; i += kWarps) rescan2(i, 3, -1);
+    } else {
+        for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1, -1);
+    }
     long long E = 0;
     if (SPEC && rank == 0) {
         unsigned long long e = 0;
@@ -632,6 +782,11 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 bAd[r] = PA.d;
                 bAj[r] = PA.j == kNoJ ? -1 : PA.j;
                 if (SPEC) { bNd[r] = PN.d; bNj[r] = PN.j == kNoJ ? -1 : PN.j; }
+                if (TOP2) {  // a's fresh row: its best only (complete iff it has none)
+                    bAd2[r] = kInf; bAj2[r] = -1;
+                    bNd2[r] = kInf; bNj2[r] = -1;
+                    cx[r] = (uint8_t)((PA.j == kNoJ ? 1 : 0) | (PN.j == kNoJ ? 2 : 0));
+                }
             }
         }
         // merge rule (engine.py:322-339): spectral wins iff d_s < w * d_a, strictly
@@ -733,15 +888,28 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (cnt[i] == 0u || i == a) continue;
             const int r = i - lo;
             int mask = 0;
-            if (bAj[r] == a || bAj[r] == b) mask |= 1;
-            if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
+            if (TOP2) {
+                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], a);
+                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], b);
+                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], a);
+                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], b);
+                if (bAj[r] < 0 && !(cx[r] & 1)) mask |= 1;
+                if (bNj[r] < 0 && !(cx[r] & 2)) mask |= 2;
+            } else {
+                if (bAj[r] == a || bAj[r] == b) mask |= 1;
+                if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
+            }
             if (mask) inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
         }
         __syncthreads();
         {
             const int ni = ninv;
             if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
-            for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
+            if (TOP2) {
+                for (int k = warp; k < ni; k += kWarps) rescan2(inv[k] >> 2, inv[k] & 3, a);
+            } else {
+                for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
+            }
         }
         __syncthreads();
         mark(4);
@@ -807,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             for (int i = 0; i < ss.nst; ++i) {
                 const uint32_t g = ss.base + i;
                 mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
-                const double* tile = ring + (size_t)(g % kStages) * (kStageBytes / 8);
+                const double* tile = ring + (size_t)(g % kStages) * (SB / 8);
                 const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
                 // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
                 // accumulate garbage that the epilogue discards via valid[])
@@ -839,8 +1007,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #endif
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
-                rowa_col<true, M>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2g, D, bAd,
-                                  bAj, bNd, bNj, pA, pN, inv, &ninv);
+                rowa_col<true, M, TOP2>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2g, D,
+                                        bAd, bAj, bNd, bNj, pA, pN, inv, &ninv,
+                                        Top2Lists{bAd2, bNd2, bAj2, bNj2, cx});
         } else {
             const int ncols = hi - lo;
             const double* mu = mu0;
@@ -892,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
-    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0);
+    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure);
     void (*kern)(SectionBatch);
 #define RHSEG_PICK(M)                                                                              \
     if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true, M> : hseg_loop_kernel<true, false, M>; \

@@ -219,7 +219,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
     const bool spec = weight > 0.0;
     auto fits = [&](int C) {
-        return hseg_loop_smem(lv.Rp, C, lv.B, spec) <= 220 * 1024 && (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
+        return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure) <= 220 * 1024 &&
+               (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
     };
     // grow the cluster until the per-CTA row slice fits shared memory
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;

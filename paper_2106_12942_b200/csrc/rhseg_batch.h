@@ -62,7 +62,7 @@ struct SectionBatch {
 // Kernel launchers (hseg_kernels.cu / section_kernels.cu). All stream-ordered.
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec);
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure);
 int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
                       int col0, int connectivity, cudaStream_t st);
