@@ -350,44 +350,6 @@ __device__ __forceinline__ void rowa_col(int jq, bool valid, bool isadj, bool ne
     else if (SPEC) cache_offer(bNd[r], bNj[r], d, a);
 }
 
-// w = 0 row-a pass: only a's neighbours need a dissimilarity (the spectral stage
-// is skipped, engine.py:326), read straight from the band-major mean cache.
-template <int NQ, int M>
-__device__ __forceinline__ void rowa_group_adj(int jbase, int lo, int hi, int a, int b, double nn,
-                                               const double* __restrict__ mu, int Rp, int B, const double* mua,
-                                               const uint32_t* cnt, const uint32_t* ra, double n2a,
-                                               const double* __restrict__ n2, double* __restrict__ D,
-                                               double* bAd, int* bAj, RowBest& pA, RowBest& pN, int* inv,
-                                               int* ninv) {
-    int j[NQ];
-    bool valid[NQ], isadj[NQ];
-    double s[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        j[q] = jbase + q * kThreads;
-        valid[q] = j[q] < hi && j[q] != a && j[q] != b && cnt[j[q]] != 0u;
-        isadj[q] = valid[q] && ((ra[j[q] >> 5] >> (j[q] & 31)) & 1u);
-        s[q] = 0.0;
-    }
-    bool any = false;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) any |= isadj[q];
-    if (any) {
-#pragma unroll 4
-        for (int k = 0; k < B; ++k) {
-            const double m = mua[k];
-            const double* row = mu + (size_t)k * Rp;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                if (isadj[q]) s[q] = acc_step<M>(s[q], m, row[j[q]]);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < NQ; ++q)
-        rowa_col<false, M>(j[q], valid[q], isadj[q], isadj[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2, D, bAd, bAj,
-                           nullptr, nullptr, pA, pN, inv, ninv);
-}
-
 // Per-CTA streaming state of the spectral row-a pass (all threads hold the same
 // values; only thread 0 issues copies).
 struct StreamState {
@@ -1011,18 +973,36 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                                         bAd, bAj, bNd, bNj, pA, pN, inv, &ninv,
                                         Top2Lists{bAd2, bNd2, bAj2, bNj2, cx});
         } else {
-            const int ncols = hi - lo;
-            const double* mu = mu0;
-            if (ncols > 2 * kThreads) {
-                for (int jb = lo + tid; jb < hi; jb += 4 * kThreads)
-                    rowa_group_adj<4, M>(jb, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA, pN,
-                                         inv, &ninv);
-            } else if (ncols > kThreads) {
-                rowa_group_adj<2, M>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA,
-                                     pN, inv, &ninv);
-            } else {
-                rowa_group_adj<1, M>(lo + tid, lo, hi, a, b, nn, mu, Rp, B, mua, cnt, ra, n2a, n2g, D, bAd, bAj, pA,
-                                     pN, inv, &ninv);
+            // w = 0: only a's (own) neighbours need d(a, j). One warp per neighbour:
+            // the lanes load j's region-major band sums coalesced, divide by the count
+            // (the exact cached mean) and the ascending-band accumulation runs through
+            // warp shuffles -- no strided, latency-bound walks over the band-major cache.
+            if (tid == 0) sScan = 0;
+            __syncthreads();
+            for (int w = tid; w < W; w += kThreads) {
+                uint32_t bits = ra[w];
+                while (bits) {
+                    const int j = (w << 5) + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    if (j >= lo && j < hi && j != b && cnt[j] != 0u) inv[atomicAdd(&sScan, 1)] = j;
+                }
+            }
+            __syncthreads();
+            const int nnb = sScan;
+            for (int t = warp; t < nnb; t += kWarps) {
+                const int j = inv[t];
+                const double* sj = sums + (size_t)j * B;
+                const double cj = (double)cnt[j];
+                double sacc = 0.0;
+                for (int k0 = 0; k0 < B; k0 += 32) {
+                    const double v = k0 + lane < B ? __ddiv_rn(sj[k0 + lane], cj) : 0.0;
+                    const int kn = min(32, B - k0);
+                    for (int kk = 0; kk < kn; ++kk)
+                        sacc = acc_step<M>(sacc, mua[k0 + kk], __shfl_sync(0xffffffffu, v, kk));
+                }
+                if (lane == 0)
+                    rowa_col<false, M>(j, true, true, true, sacc, nn, a, b, lo, Rp, cnt, n2a, n2g, D, bAd, bAj, nullptr,
+                                       nullptr, pA, pN, inv, &ninv);
             }
         }
         pA = block_min_rb(pA, rscr);
