@@ -368,6 +368,7 @@ struct StreamState {
 template <bool CLUSTER, bool SPEC, int M>
 __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
+    const long long t_entry = clock64();
     const int C = CLUSTER ? bt.C : 1;
     const int rank = CLUSTER ? (int)cluster_rank() : 0;
     const int sec = bt.sec0 + (int)(blockIdx.x / C);
@@ -681,8 +682,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int a_prev = -1, step = 0, conv = 0;
     long long pairs = 0;
     // optional per-phase cycle accounting (RHSEG_PROFILE=1): thread 0 of every CTA
-    unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tmark = clock64();
+    pc[6] = (unsigned long long)(tmark - t_entry);  // prologue (caches, initial rescans, E)
     auto mark = [&](int ph) {
         if (bt.prof && tid == 0) {
             const long long t = clock64();
@@ -1027,12 +1029,14 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (!RHSEG_EARLY_STREAM && SPEC && R0 - step > target) begin_stream();
     }
     if (CLUSTER) cluster_barrier();  // keep our slots alive until every peer is done reading
+    if (bt.prof && tid == 0) {
+        pc[7] = (unsigned long long)(clock64() - t_entry);  // whole kernel
+        for (int q = 0; q < 8; ++q) atomicAdd(bt.prof + q, pc[q]);
+    }
     if (rank == 0) {
         for (int i = tid; i < Rp; i += kThreads) bt.count[(size_t)sec * Rp + i] = cnt[i];
         if (tid == 0) {
             bt.nlog[sec] = step;
-            if (bt.prof)
-                for (int q = 0; q < 6; ++q) atomicAdd(bt.prof + q, pc[q]);
             bt.conv[sec] = conv;
             if (bt.pairs) bt.pairs[sec] = pairs;
         }

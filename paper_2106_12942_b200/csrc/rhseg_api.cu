@@ -382,13 +382,15 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
         for (int s = 0; s < lv.nsec; ++s) steps += lv.nlogh[s];
         const double tot = (double)(ph[0] + ph[1] + ph[2] + ph[3] + ph[4]) + 1e-9;
         fprintf(stderr,
-                "[rhseg profile] level %d: %d sections x C=%d, Rp=%d, %lld steps, %.0f cycles/step/CTA: "
+                "[rhseg profile] level %d: %d sections x C=%d, Rp=%d, %lld steps, %.0f cycles/step (per CTA): "
                 "argmin %.1f%% combine %.1f%% merge %.1f%% row-a %.1f%% rescan %.1f%%, %.2f rescans/step\n",
                 lv.level, lv.nsec, lv.C, lv.Rp, steps, tot / (double)std::max(1LL, steps) / lv.C,
                 100 * ph[0] / tot, 100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot,
                 (double)ph[5] / (double)std::max(1LL, steps));
         cudaFree(prof);
-        fprintf(stderr, "[rhseg profile] level %d host wall in run_level %.2f ms\n", lv.level, now_ms() - t_enter);
+        fprintf(stderr, "[rhseg profile] level %d host wall in run_level %.2f ms; per CTA: prologue %.0f cycles, "
+                "kernel %.0f cycles\n", lv.level, now_ms() - t_enter, (double)ph[6] / (lv.nsec * lv.C),
+                (double)ph[7] / (lv.nsec * lv.C));
     }
     lv.done = true;
     return RHSEG_OK;
