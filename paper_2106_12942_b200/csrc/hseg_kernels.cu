@@ -207,7 +207,7 @@ constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
-    size_t slot, rslot, pscr, rscr, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -217,9 +217,10 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     LoopSmem L;
     size_t o = 0;
     L.slot = o;  o += 2 * sizeof(Slot);
-    L.rslot = o; o += kMaxCluster * sizeof(Slot);
+    L.rslot = o; o += 2 * kMaxCluster * sizeof(Slot);  // [step parity][source CTA]
     L.pscr = o;  o += kWarps * sizeof(Pair);
     L.rscr = o;  o += kWarps * sizeof(RowBest);
+    L.spart = o; o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
     L.bars = o;  o += 2 * kStages * 8;  // full[kStages], empty[kStages]
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
     RowBest* rscr = reinterpret_cast<RowBest*>(smem + L.rscr);
+    RowBest* spart = reinterpret_cast<RowBest*>(smem + L.spart);
     int* misc = reinterpret_cast<int*>(smem + L.misc);
     int& ninv = misc[0];
     int& sdE = misc[1];
@@ -714,23 +716,27 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             slot[par].rpA = rpart[0];
             slot[par].rpN = rpart[1];
         }
-        if (CLUSTER) cluster_barrier();
-        else __syncthreads();
+        if (CLUSTER) {
+            // push this CTA's slot into rslot[par][rank] of every CTA of the cluster
+            // (fire-and-forget DSMEM stores); after the release/acquire cluster
+            // barrier every CTA combines the C slots from its own shared memory
+            __syncthreads();
+            if (tid < C * 16) {
+                const int r = tid >> 4, w = tid & 15;
+                const uint32_t v = reinterpret_cast<const uint32_t*>(&slot[par])[w];
+                dsmem_st_u32(dsmem_addr(&rslot[par * kMaxCluster + rank], (unsigned)r) + 4u * w, v);
+            }
+            cluster_barrier();
+        } else {
+            __syncthreads();
+        }
 
         mark(0);
         // (B) combine the C slots: identical decision in every CTA
-        if (CLUSTER) {
-            if (tid < C * 16) {
-                const int r = tid >> 4, w = tid & 15;
-                reinterpret_cast<uint32_t*>(&rslot[r])[w] =
-                    dsmem_ld_u32(dsmem_addr(&slot[par], (unsigned)r) + 4u * w);
-            }
-            __syncthreads();
-        }
         Pair A = pair_none(), N = pair_none();
         RowBest PA = rb_none(), PN = rb_none();
         for (int r = 0; r < C; ++r) {
-            const Slot& s = CLUSTER ? rslot[r] : slot[par];
+            const Slot& s = CLUSTER ? rslot[par * kMaxCluster + r] : slot[par];
             pair_offer(A, s.selA);
             rb_offer(PA, s.rpA.d, s.rpA.j);
             if (SPEC) {
@@ -871,6 +877,57 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
             if (TOP2) {
                 for (int k = warp; k < ni; k += kWarps) rescan2(inv[k] >> 2, inv[k] & 3, a);
+            } else if (CLUSTER) {
+                // big sections: every warp takes a slice of the row, so one rescan
+                // costs one round of loads instead of R0/256 sequential ones
+                const int per = (((R0 + kWarps - 1) / kWarps) + 31) & ~31;
+                const int c0 = min(R0, warp * per), c1 = min(R0, c0 + per);
+                for (int k = 0; k < ni; ++k) {
+                    const int i = inv[k] >> 2, mask = inv[k] & 3;
+                    RowBest ba = rb_none(), bn = rb_none();
+                    const uint32_t* arow = adj + (size_t)i * W;
+                    const double* drow = D + (size_t)i * Rp;
+                    for (int j0 = c0; j0 < c1; j0 += 32 * 16) {
+                        double dv[16];
+                        uint32_t wv[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int j = j0 + 32 * u + lane;
+                            dv[u] = j < c1 ? __ldcs(drow + j) : kInf;
+                            wv[u] = (j0 + 32 * u) < c1 ? arow[(j0 >> 5) + u] : 0u;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int j = j0 + 32 * u + lane;
+                            if (j < c1 && j != i && j != a && cnt[j] != 0u) {
+                                if ((wv[u] >> lane) & 1u) {
+                                    if (mask & 1) rb_offer(ba, dv[u], j);
+                                } else if (SPEC && (mask & 2)) {
+                                    rb_offer(bn, dv[u], j);
+                                }
+                            }
+                        }
+                    }
+                    ba = warp_min_rb(ba);
+                    if (SPEC) bn = warp_min_rb(bn);
+                    RowBest* part = rscr;  // kWarps entries per stage (rscr + rpart area)
+                    if (lane == 0) {
+                        part[warp] = ba;
+                        if (SPEC) spart[warp] = bn;
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        RowBest fa = rb_none(), fn = rb_none();
+                        for (int w = 0; w < kWarps; ++w) {
+                            rb_offer(fa, part[w].d, part[w].j);
+                            if (SPEC) rb_offer(fn, spart[w].d, spart[w].j);
+                        }
+                        const int r = i - lo;
+                        if (mask & 1) { bAd[r] = fa.d; bAj[r] = fa.j == kNoJ ? -1 : fa.j; }
+                        if (SPEC && (mask & 2)) { bNd[r] = fn.d; bNj[r] = fn.j == kNoJ ? -1 : fn.j; }
+                    }
+                    __syncthreads();
+                }
             } else {
                 for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
             }
