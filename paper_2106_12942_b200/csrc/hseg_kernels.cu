@@ -24,6 +24,8 @@
 // one barrier.cluster (double-buffered by step parity).
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "rhseg_batch.h"
 #include "rhseg_device.cuh"
 
@@ -177,6 +179,13 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
 // per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
+#ifndef RHSEG_F32FILTER
+#define RHSEG_F32FILTER 1  // stream fp32 filter means (exact fp64 re-evaluation) when w > 0
+#endif
+#if defined(RHSEG_DIRECT) && RHSEG_DIRECT
+#undef RHSEG_F32FILTER
+#define RHSEG_F32FILTER 0  // the unstaged experiment streams fp64 only
+#endif
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -207,12 +216,12 @@ constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
-    size_t slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t fref, fxa, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
-__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2) {
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2, bool f32) {
     const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
     size_t o = 0;
@@ -231,8 +240,10 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.bNj = o;   o = align16(o + Rs * 4);
     L.inv = o;   o = align16(o + Rs * 4);
     L.cnt = o;   o = align16(o + (size_t)Rp * 4);
-    L.col = o;   o = align16(o + (spec ? Rs * 4 : 0));
-    L.slot_of = o; o = align16(o + (spec ? Rs * 4 : 0));
+    L.col = o;   o = align16(o + (spec ? Rs * 2 : 0));      // int16: region ids < 16384
+    L.slot_of = o; o = align16(o + (spec ? Rs * 2 : 0));
+    L.fref = o;  o = align16(o + (f32 ? (size_t)B * 4 : 0));  // F32: centring reference (fp32)
+    L.fxa = o;   o = align16(o + (f32 ? (size_t)B * 4 : 0));  // F32: a's centred fp32 mean
     L.bAd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
     L.bNd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
     L.bAj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
@@ -245,9 +256,13 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     return L;
 }
 __host__ __device__ inline bool use_top2(bool spec, int C, int measure) { return spec && C == 1 && measure == kSam; }
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure) {
-    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure)).total;
+__host__ __device__ inline bool use_f32(bool spec, int C, int measure) {
+    return RHSEG_F32FILTER && spec && C == 1 && measure != kSam;
 }
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure) {
+    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure)).total;
+}
+bool hseg_use_f32(bool spec, int C, int measure) { return use_f32(spec, C, measure); }
 int hseg_loop_max_rows() { return kMaxSlots; }
 
 __device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j) {
@@ -322,6 +337,74 @@ struct Top2Lists {
     uint8_t* cx;
 };
 
+// ---- F32 filter (w > 0, BSMSE/Euclidean, one CTA per section) ---------------
+// The stream carries x = fl32(mu - ref) (ref: the section's region-0 mean at loop
+// start) instead of the fp64 means: half the bytes. Every dissimilarity the
+// merge sequence depends on is still the exact fp64 reference value: the fp32
+// sum only yields a rigorous interval [dlo, dhi] around the reference's d, and
+// every comparison the interval cannot settle is re-evaluated exactly (one warp,
+// means from the region-major fp64 band sums). Interval derivation: with
+// N = ||x||_2 bounds, |e| <= u32'|x| per band, eta = u(N_a+N_j) + u64||t~||,
+// |s~ - S| <= g s~ + 2 eta sqrt(s~) + eta^2 (g = (2B+16) u64 covers the fp64
+// accumulation of s~ and of the reference's own s), then directed-rounding
+// sqrt(coef * s_lo/hi) with a final (1 -/+ 8e-16).
+template <int M>
+__device__ __forceinline__ void f32_interval(double st, double nsum, double ni, double nj, int B, double& dlo,
+                                             double& dhi) {
+    const double u = 5.97e-8;                                  // 2^-24 (1 + 1.6e-3)
+    const double g = (2.0 * B + 16.0) * 1.1102230246251565e-16;  // fp64 accumulation
+    const double rt = sqrt(st);
+    const double eta = u * nsum + 1.2e-16 * rt + 1e-43;
+    double err = g * st + 2.0 * eta * rt + eta * eta;
+    err = (err + g * (st + err)) * 1.01;
+    const double slo = fmax(0.0, st - err), shi = st + err;
+    if (M == kBsmse) {
+        const double coef = __ddiv_rn(__dmul_rn(ni, nj), __dadd_rn(ni, nj));
+        dlo = __dsqrt_rd(__dmul_rd(coef, slo)) * (1.0 - 8e-16);
+        dhi = __dsqrt_ru(__dmul_ru(coef, shi)) * (1.0 + 8e-16);
+    } else {
+        dlo = __dsqrt_rd(slo) * (1.0 - 8e-16);
+        dhi = __dsqrt_ru(shi) * (1.0 + 8e-16);
+    }
+}
+// D entries: exact values are >= 0 doubles; an interval is stored as
+// [sign=1 | float(dlo) rounded down | float(dhi) rounded up].
+__device__ __forceinline__ double d_pack_interval(double dlo, double dhi) {
+    const unsigned long long lo = __float_as_uint(__double2float_rd(dlo));
+    const unsigned long long hi = __float_as_uint(__double2float_ru(dhi));
+    return __longlong_as_double((long long)((1ULL << 63) | (lo << 32) | hi));
+}
+__device__ __forceinline__ bool d_is_interval(double v) { return __double_as_longlong(v) < 0; }
+__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    if ((long long)b < 0) {
+        lo = (double)__uint_as_float((uint32_t)(b >> 32) & 0x7fffffffu);
+        hi = (double)__uint_as_float((uint32_t)b);
+    } else {
+        lo = hi = v;
+    }
+}
+// Exact d(i, j) by one warp (all lanes return it): means from the region-major
+// fp64 band sums (sums[r][k] / count[r], the exact cached values), or from an
+// fp64 mean vector in shared memory; ascending-band accumulation via shuffles.
+template <int M>
+__device__ __forceinline__ double warp_exact(const double* mi_smem, const double* si, double ci, const double* sj,
+                                             double cj, int B, int lane) {
+    double s = 0.0;
+    for (int k0 = 0; k0 < B; k0 += 32) {
+        const int k = k0 + lane;
+        double vi = 0.0, vj = 0.0;
+        if (k < B) {
+            vi = mi_smem ? mi_smem[k] : __ddiv_rn(si[k], ci);
+            vj = __ddiv_rn(sj[k], cj);
+        }
+        const int kn = min(32, B - k0);
+        for (int kk = 0; kk < kn; ++kk)
+            s = acc_step<M>(s, __shfl_sync(0xffffffffu, vi, kk), __shfl_sync(0xffffffffu, vj, kk));
+    }
+    return pair_finish<M>(ci, cj, s, 0.0, 0.0);
+}
+
 // Epilogue for one column j of the row-a pass: D row/column update, offer
 // (d, a) to row j's caches, mark rows whose cached partner died.
 template <bool SPEC, int M, bool TOP2 = false>
@@ -381,8 +464,11 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
 
     constexpr bool TOP2 = SPEC && !CLUSTER && M == kSam;
+    constexpr bool F32 = RHSEG_F32FILTER && SPEC && !CLUSTER && M != kSam;
+    using SE = typename std::conditional<F32, float, double>::type;  // streamed element
+    constexpr int ES = (int)sizeof(SE);
     constexpr int SB = TOP2 ? kStageBytesTop2 : kStageBytes;
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2);
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -403,8 +489,10 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int* bNj = reinterpret_cast<int*>(smem + L.bNj);
     int* inv = reinterpret_cast<int*>(smem + L.inv);
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
-    int* col = reinterpret_cast<int*>(smem + L.col);
-    int* slot_of = reinterpret_cast<int*>(smem + L.slot_of);
+    short* col = reinterpret_cast<short*>(smem + L.col);
+    short* slot_of = reinterpret_cast<short*>(smem + L.slot_of);
+    float* fref = reinterpret_cast<float*>(smem + L.fref);
+    float* fxa = reinterpret_cast<float*>(smem + L.fxa);
     // TOP2: second-best partner per row and stage + "list holds every candidate" bits
     double* bAd2 = reinterpret_cast<double*>(smem + L.bAd2);
     double* bNd2 = reinterpret_cast<double*>(smem + L.bNd2);
@@ -414,7 +502,10 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
     double* const mu0 = bt.mu + sec * bt.mu_stride();
-    double* const mu1 = SPEC ? bt.mu2 + sec * bt.mu_stride() : nullptr;
+    double* const mu1 = (SPEC && !F32) ? bt.mu2 + sec * bt.mu_stride() : nullptr;
+    // the streamed mean buffers: fp64 mu / mu2, or the centred fp32 copies (F32)
+    SE* const sb0 = reinterpret_cast<SE*>(F32 ? (void*)(bt.mu32 + sec * bt.mu_stride()) : (void*)mu0);
+    SE* const sb1 = reinterpret_cast<SE*>(F32 ? (void*)(bt.mu32b + sec * bt.mu_stride()) : (void*)mu1);
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
@@ -500,6 +591,93 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
     };
 
+    // F32 rescan: D rows hold exact values and intervals. Pass 1: exact best and
+    // smallest interval top per stage; pass 2: every interval that could still
+    // win (lo <= that bound) is evaluated exactly by the warp and written back.
+    auto rescanf = [&](int i, int mask, int ex) {
+        RowBest ba = rb_none(), bn = rb_none();
+        double ua = kInf, un = kInf;
+        const uint32_t* arow = adj + (size_t)i * W;
+        double* drow = D + (size_t)i * Rp;
+        const bool live_i = cnt[i] != 0u;
+        constexpr int U = 16;
+        if (live_i) {
+            for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                double dv[U];
+                int jv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int sl = s0 + 32 * u + lane;
+                    const int j = sl < ss.S ? col[sl] : -1;
+                    jv[u] = j;
+                    dv[u] = j >= 0 ? __ldcs(drow + j) : kInf;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = jv[u];
+                    if (j < 0 || j == i || j == ex || cnt[j] == 0u) continue;
+                    const bool aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                    if (aj ? !(mask & 1) : !(mask & 2)) continue;
+                    double lo2, hi2;
+                    d_unpack(dv[u], lo2, hi2);
+                    if (d_is_interval(dv[u])) {
+                        if (aj) ua = fmin(ua, hi2);
+                        else un = fmin(un, hi2);
+                    } else if (aj) {
+                        rb_offer(ba, dv[u], j);
+                    } else {
+                        rb_offer(bn, dv[u], j);
+                    }
+                }
+            }
+        }
+        ba = warp_min_rb(ba);
+        bn = warp_min_rb(bn);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            ua = fmin(ua, __shfl_xor_sync(0xffffffffu, ua, o));
+            un = fmin(un, __shfl_xor_sync(0xffffffffu, un, o));
+        }
+        const double bndA = fmin(ba.d, ua), bndN = fmin(bn.d, un);
+        if (live_i && (ua < kInf || un < kInf)) {
+            const double* si = sums + (size_t)i * B;
+            const double ci = (double)cnt[i];
+            for (int s0 = 0; s0 < ss.S; s0 += 32) {
+                const int sl = s0 + lane;
+                const int j = sl < ss.S ? col[sl] : -1;
+                bool cand = false, aj = false;
+                if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                    aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                    const double v = __ldcs(drow + j);
+                    if ((aj ? (mask & 1) : (mask & 2)) && d_is_interval(v)) {
+                        double lo2, hi2;
+                        d_unpack(v, lo2, hi2);
+                        cand = lo2 <= (aj ? bndA : bndN);
+                    }
+                }
+                unsigned m = __ballot_sync(0xffffffffu, cand);
+                while (m) {
+                    const int src = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int jj = __shfl_sync(0xffffffffu, j, src);
+                    const bool ajj = __shfl_sync(0xffffffffu, aj, src);
+                    const double d = warp_exact<M>(nullptr, si, ci, sums + (size_t)jj * B, (double)cnt[jj], B, lane);
+                    if (lane == 0) {
+                        drow[jj] = d;
+                        D[(size_t)jj * Rp + i] = d;
+                    }
+                    if (ajj) rb_offer(ba, d, jj);
+                    else rb_offer(bn, d, jj);
+                }
+            }
+        }
+        if (lane == 0) {
+            const int r = i - lo;
+            if (mask & 1) { bAd[r] = ba.d; bAj[r] = ba.j == kNoJ ? -1 : ba.j; }
+            if (mask & 2) { bNd[r] = bn.d; bNj[r] = bn.j == kNoJ ? -1 : bn.j; }
+        }
+    };
+
     // TOP2 rescan: the two best candidates per masked stage + the complete bit,
     // over the compacted live-column list (one CTA owns every column).
     auto rescan2 = [&](int i, int mask, int ex) {
@@ -559,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         const int sl = (int)(abs_stage % kStages);
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
-        const uint32_t rowb = (uint32_t)ss.S2 * 8u;
+        const uint32_t rowb = (uint32_t)ss.S2 * (uint32_t)ES;
         if (RHSEG_EMPTY_BARRIERS && abs_stage >= (uint32_t)kStages)
             mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
         if (lane == 0) {
@@ -568,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
         __syncwarp();
         char* dst = reinterpret_cast<char*>(ring) + (size_t)sl * SB;
-        const double* src = (ss.cur ? mu1 : mu0) + lo;
+        const SE* src = (ss.cur ? sb1 : sb0) + lo;
         for (int kk = lane; kk < kb; kk += 32)
             bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
         if (kPrefetchBytes > 0) {
@@ -606,8 +784,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             const int id = s < ss.S ? col[s] : -1;
             int tot;
             const int np = base + block_scan(id >= 0 ? 1 : 0, tot);
-            const double* src = (ss.cur ? mu1 : mu0) + lo + s;
-            double* dst = (ss.cur ? mu0 : mu1) + lo + np;
+            const SE* src = (ss.cur ? sb1 : sb0) + lo + s;
+            SE* dst = (ss.cur ? sb0 : sb1) + lo + np;
             if (id >= 0) {
 #pragma unroll 8
                 for (int k = 0; k < B; ++k) dst[(size_t)k * Rp] = src[(size_t)k * Rp];
@@ -628,12 +806,13 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // (compacting first when >= 25% of the own columns are holes).
     auto begin_stream = [&]() {
         if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
-        ss.S2 = (ss.S + 1) & ~1;
-        ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * 8))) : B;
+        constexpr int kAlign = 16 / ES;  // bulk copies move multiples of 16 bytes
+        ss.S2 = (ss.S + kAlign - 1) / kAlign * kAlign;
+        ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * ES))) : B;
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
         ss.pf = 0;
-        ss.PF = (ss.S2 > 0 && kPrefetchBytes > 0) ? min(B, max(1, kPrefetchBytes / (ss.S2 * 8))) : 0;
+        ss.PF = (ss.S2 > 0 && kPrefetchBytes > 0) ? min(B, max(1, kPrefetchBytes / (ss.S2 * ES))) : 0;
         const int pre = RHSEG_DIRECT ? 0 : min(kStages, ss.nst);
         if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
@@ -664,10 +843,29 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         rpart[1] = rb_none();
     }
     __syncthreads();
+    if (F32) {
+        // centre on region 0's mean (rounded to fp32), fp32 stream copy + norm bounds
+        for (int k = tid; k < B; k += kThreads) fref[k] = __double2float_rn(mu0[(size_t)k * Rp]);
+        __syncthreads();
+        for (int sl = tid; sl < hi - lo; sl += kThreads) {
+            const int j = lo + sl;
+            double nrm = 0.0;
+            for (int k = 0; k < B; ++k) {
+                const float x = __double2float_rn(__dsub_rn(mu0[(size_t)k * Rp + j], (double)fref[k]));
+                sb0[(size_t)k * Rp + j] = (SE)x;
+                nrm += (double)x * (double)x;
+            }
+            bt.xnorm[(size_t)sec * Rp + j] = sqrt(nrm) * (1.0 + 1e-6) + 1e-300;
+        }
+        fence_proxy_async_global();
+        __syncthreads();
+    }
     if (TOP2) {
         for (int r = tid; r < hi - lo; r += kThreads) cx[r] = 0;
         __syncthreads();
         for (int i = lo + warp; i < hi; i += kWarps) rescan2(i, 3, -1);
+    } else if (F32) {
+        for (int i = lo + warp; i < hi; i += kWarps) rescanf(i, 3, -1);
     } else {
         for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1, -1);
     }
@@ -786,14 +984,20 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         {
             double* sa = sums + (size_t)a * B;
             const double* sb = sums + (size_t)b * B;
-            double* mu_a = SPEC ? (own_a ? (ss.cur ? mu1 : mu0) + lo + slot_of[a - lo] : nullptr)
-                                : mu0 + a;
+            SE* mu_a = SPEC ? (own_a ? (ss.cur ? sb1 : sb0) + lo + slot_of[a - lo] : nullptr)
+                            : reinterpret_cast<SE*>(mu0 + a);
             for (int k = tid; k < B; k += kThreads) {
                 const double s = __dadd_rn(sa[k], sb[k]);
                 sa[k] = s;
                 const double m = __ddiv_rn(s, nn);
                 mua[k] = m;
-                if (own_a) mu_a[(size_t)k * Rp] = m;
+                if (F32) {
+                    const float x = __double2float_rn(__dsub_rn(m, (double)fref[k]));
+                    fxa[k] = x;
+                    if (own_a) mu_a[(size_t)k * Rp] = (SE)x;
+                } else if (own_a) {
+                    mu_a[(size_t)k * Rp] = (SE)m;
+                }
             }
             if (SPEC && own_a) fence_proxy_async_global();
         }
@@ -928,6 +1132,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     }
                     __syncthreads();
                 }
+            } else if (F32) {
+                for (int k = warp; k < ni; k += kWarps) rescanf(inv[k] >> 2, inv[k] & 3, a);
             } else {
                 for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
             }
@@ -936,7 +1142,23 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
-        double n2a = 0.0;
+        double n2a = 0.0, xna = 0.0;
+        if (F32) {  // ||x_a|| upper bound (any summation order: it only widens intervals)
+            double* sx = reinterpret_cast<double*>(misc + 8);
+            if (warp == 0) {
+                double v = 0.0;
+                for (int k = lane; k < B; k += 32) v += (double)fxa[k] * (double)fxa[k];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) {
+                    *sx = sqrt(v) * (1.0 + 1e-6) + 1e-300;
+                    if (own_a) bt.xnorm[(size_t)sec * Rp + a] = *sx;
+                }
+            }
+            if (tid == 0) sScan = 0;
+            __syncthreads();
+            xna = *sx;
+        }
         if (M == kSam) {  // squared norm of a's new mean, sequential (oracle order)
             double* sn2a = reinterpret_cast<double*>(misc + 6);
             if (tid == 0) {
@@ -996,7 +1218,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             for (int i = 0; i < ss.nst; ++i) {
                 const uint32_t g = ss.base + i;
                 mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
-                const double* tile = ring + (size_t)(g % kStages) * (SB / 8);
+                const SE* tile = reinterpret_cast<const SE*>(ring) + (size_t)(g % kStages) * (SB / ES);
                 const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
                 // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
                 // accumulate garbage that the epilogue discards via valid[])
@@ -1004,9 +1226,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #define RHSEG_CONSUME(NQC)                                                        \
     case NQC:                                                                     \
         for (int kk = 0; kk < kb; ++kk) {                                         \
-            const double m = mua[k0 + kk];                                        \
-            const double* row = tile + (size_t)kk * ss.S2 + tid;                  \
-            _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, row[q * kThreads]); \
+            const double m = F32 ? (double)fxa[k0 + kk] : mua[k0 + kk];           \
+            const SE* row = tile + (size_t)kk * ss.S2 + tid;                      \
+            _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, (double)row[q * kThreads]); \
         }                                                                         \
         break;
                     RHSEG_CONSUME(1) RHSEG_CONSUME(2) RHSEG_CONSUME(3) RHSEG_CONSUME(4)
@@ -1026,11 +1248,68 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             }
             ss.issued += max(0, ss.nst - kStages);
 #endif
+            if (F32) {
+                // intervals around every d(a, j); exact re-evaluation only where an
+                // interval cannot settle a comparison: row j's cached best, or a's
+                // own minimum (any column whose dlo reaches below min dhi)
+                const double* xn = bt.xnorm + (size_t)sec * Rp;
+                double dlo[NQ], dhi[NQ];
+                double uA = kInf, uN = kInf;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                rowa_col<true, M, TOP2>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2g, D,
-                                        bAd, bAj, bNd, bNj, pA, pN, inv, &ninv,
-                                        Top2Lists{bAd2, bNd2, bAj2, bNj2, cx});
+                for (int q = 0; q < NQ; ++q) {
+                    dlo[q] = kInf;
+                    dhi[q] = kInf;
+                    if (valid[q]) {
+                        f32_interval<M>(s[q], xna + xn[jq[q]], nn, (double)cnt[jq[q]], B, dlo[q], dhi[q]);
+                        if (isadj[q]) uA = fmin(uA, dhi[q]);
+                        else uN = fmin(uN, dhi[q]);
+                    }
+                }
+                {
+                    RowBest ra2 = block_min_rb(RowBest{uA, 0}, rscr);
+                    RowBest rn2 = block_min_rb(RowBest{uN, 0}, rscr);
+                    uA = ra2.d;
+                    uN = rn2.d;
+                }
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    if (!valid[q]) continue;
+                    const int j = jq[q], r = j - lo;
+                    const double bd = isadj[q] ? bAd[r] : bNd[r];
+                    if (dlo[q] <= bd || dlo[q] <= (isadj[q] ? uA : uN)) {
+                        inv[atomicAdd(&sScan, 1)] = (j << 1) | (isadj[q] ? 1 : 0);
+                    } else {
+                        const double v = d_pack_interval(dlo[q], dhi[q]);
+                        D[(size_t)j * Rp + a] = v;
+                        D[(size_t)a * Rp + j] = v;
+                    }
+                }
+                __syncthreads();
+                const int nex = sScan;
+                for (int t = warp; t < nex; t += kWarps) {
+                    const int j = inv[t] >> 1;
+                    const bool adjj = inv[t] & 1;
+                    const double d = warp_exact<M>(mua, nullptr, nn, sums + (size_t)j * B, (double)cnt[j], B, lane);
+                    if (lane == 0) {
+                        D[(size_t)j * Rp + a] = d;
+                        D[(size_t)a * Rp + j] = d;
+                        const int r = j - lo;
+                        if (adjj) {
+                            rb_offer(pA, d, j);
+                            cache_offer(bAd[r], bAj[r], d, a);
+                        } else {
+                            rb_offer(pN, d, j);
+                            cache_offer(bNd[r], bNj[r], d, a);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    rowa_col<true, M, TOP2>(jq[q], valid[q], isadj[q], valid[q], s[q], nn, a, b, lo, Rp, cnt, n2a, n2g,
+                                            D, bAd, bAj, bNd, bNj, pA, pN, inv, &ninv,
+                                            Top2Lists{bAd2, bNd2, bAj2, bNj2, cx});
+            }
         } else {
             // w = 0: only a's (own) neighbours need d(a, j). One warp per neighbour:
             // the lanes load j's region-major band sums coalesced, divide by the count

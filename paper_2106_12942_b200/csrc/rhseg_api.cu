@@ -247,7 +247,10 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     o = 0;
     const size_t oAdj = take(ns * C * Rp * W * 4);
     lv.work_zero = o;
-    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec ? ns * B * Rp * 8 : 0),
+    const bool f32 = hseg_use_f32(spec, lv.C, lv.measure);
+    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec && !f32 ? ns * B * Rp * 8 : 0),
+                 oM32 = take(f32 ? ns * B * Rp * 4 : 0), oM32b = take(f32 ? ns * B * Rp * 4 : 0),
+                 oXn = take(f32 ? ns * Rp * 8 : 0),
                  oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
     {
@@ -284,7 +287,10 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.pairs = reinterpret_cast<long long*>(K + oPr);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
-    b.mu2 = spec ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.mu2 = spec && !f32 ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.mu32 = f32 ? reinterpret_cast<float*>(Wk + oM32) : nullptr;
+    b.mu32b = f32 ? reinterpret_cast<float*>(Wk + oM32b) : nullptr;
+    b.xnorm = f32 ? reinterpret_cast<double*>(Wk + oXn) : nullptr;
     b.sums = reinterpret_cast<double*>(Wk + oSums);
     lv.map = reinterpret_cast<int*>(K + oMap);
     CK(cudaMemcpyAsync(const_cast<int*>(b.R0), lv.R0h.data(), ns * 4, cudaMemcpyHostToDevice, st));

@@ -36,6 +36,9 @@ struct SectionBatch {
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
     double* mu;
     double* nrm2;        // [nsec][Rp] squared norm of each mean vector (sam only, else nullptr)
+    float* mu32;         // F32 filter: [nsec][B][Rp] centred fp32 means (compacted stream), ping-pong
+    float* mu32b;        //   second buffer of the ping-pong
+    double* xnorm;       //   [nsec][Rp] upper bound of ||centred fp32 mean||_2 per region
     double* mu2;         // second mean buffer: the loop kernel compacts live columns into it (w > 0)
     double* D;
     double* sums;
@@ -64,6 +67,7 @@ void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
 size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure);
 int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
+bool hseg_use_f32(bool spec, int C, int measure);  // the loop streams fp32 filter means
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
                       int col0, int connectivity, cudaStream_t st);
 void launch_resolve(const SectionBatch& b, cudaStream_t st);
