@@ -591,15 +591,16 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
     };
 
-    // F32 rescan: D rows hold exact values and intervals. Pass 1: exact best and
-    // smallest interval top per stage; pass 2: every interval that could still
-    // win (lo <= that bound) is evaluated exactly by the warp and written back.
+    // F32 rescan: D rows hold exact values and intervals; the row's best may be
+    // cached as an interval. Pass 1: per stage the smallest upper bound U (and
+    // the entry holding it); pass 2: entries with lower bound <= U are the only
+    // possible minima -- one such entry is cached as it is, several are resolved
+    // exactly (intervals evaluated by the warp, written back to D).
     auto rescanf = [&](int i, int mask, int ex) {
-        RowBest ba = rb_none(), bn = rb_none();
-        double ua = kInf, un = kInf;
         const uint32_t* arow = adj + (size_t)i * W;
         double* drow = D + (size_t)i * Rp;
         const bool live_i = cnt[i] != 0u;
+        double uA = kInf, uN = kInf;  // min upper bound per stage
         constexpr int U = 16;
         if (live_i) {
             for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
@@ -620,42 +621,63 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     if (aj ? !(mask & 1) : !(mask & 2)) continue;
                     double lo2, hi2;
                     d_unpack(dv[u], lo2, hi2);
-                    if (d_is_interval(dv[u])) {
-                        if (aj) ua = fmin(ua, hi2);
-                        else un = fmin(un, hi2);
-                    } else if (aj) {
-                        rb_offer(ba, dv[u], j);
-                    } else {
-                        rb_offer(bn, dv[u], j);
-                    }
+                    if (aj) uA = fmin(uA, hi2);
+                    else uN = fmin(uN, hi2);
                 }
             }
         }
-        ba = warp_min_rb(ba);
-        bn = warp_min_rb(bn);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            ua = fmin(ua, __shfl_xor_sync(0xffffffffu, ua, o));
-            un = fmin(un, __shfl_xor_sync(0xffffffffu, un, o));
+            uA = fmin(uA, __shfl_xor_sync(0xffffffffu, uA, o));
+            uN = fmin(uN, __shfl_xor_sync(0xffffffffu, uN, o));
         }
-        const double bndA = fmin(ba.d, ua), bndN = fmin(bn.d, un);
-        if (live_i && (ua < kInf || un < kInf)) {
+        // pass 2: candidates (lo <= U). A stage with one candidate caches it as it
+        // is; a stage with several takes their exact lexicographic minimum
+        // (intervals evaluated by the warp and written back to D).
+        RowBest ba = rb_none(), bn = rb_none();   // exact minima
+        RowBest sa = rb_none(), sn = rb_none();   // the single candidate (packed value, j)
+        int na = 0, nbn = 0;
+        auto candidate = [&](int j, bool& aj, double& v) {
+            aj = false;
+            v = kInf;
+            if (j < 0 || j == i || j == ex || cnt[j] == 0u) return false;
+            aj = (arow[j >> 5] >> (j & 31)) & 1u;
+            if (aj ? !(mask & 1) : !(mask & 2)) return false;
+            v = __ldcs(drow + j);
+            double lo2, hi2;
+            d_unpack(v, lo2, hi2);
+            return lo2 <= (aj ? uA : uN);
+        };
+        if (live_i && (uA < kInf || uN < kInf)) {
+            for (int s0 = 0; s0 < ss.S; s0 += 32) {
+                const int sl = s0 + lane;
+                bool aj;
+                double v;
+                const int j = sl < ss.S ? col[sl] : -1;
+                const bool cand = candidate(j, aj, v);
+                na += __popc(__ballot_sync(0xffffffffu, cand && aj));
+                nbn += __popc(__ballot_sync(0xffffffffu, cand && !aj));
+                if (cand) {
+                    if (aj) sa = RowBest{v, j};
+                    else sn = RowBest{v, j};
+                }
+            }
+        }
+        if (na > 1 || nbn > 1) {
             const double* si = sums + (size_t)i * B;
             const double ci = (double)cnt[i];
             for (int s0 = 0; s0 < ss.S; s0 += 32) {
                 const int sl = s0 + lane;
+                bool aj;
+                double v;
                 const int j = sl < ss.S ? col[sl] : -1;
-                bool cand = false, aj = false;
-                if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
-                    aj = (arow[j >> 5] >> (j & 31)) & 1u;
-                    const double v = __ldcs(drow + j);
-                    if ((aj ? (mask & 1) : (mask & 2)) && d_is_interval(v)) {
-                        double lo2, hi2;
-                        d_unpack(v, lo2, hi2);
-                        cand = lo2 <= (aj ? bndA : bndN);
-                    }
+                bool cand = candidate(j, aj, v);
+                cand = cand && (aj ? na > 1 : nbn > 1);
+                if (cand && !d_is_interval(v)) {
+                    if (aj) rb_offer(ba, v, j);
+                    else rb_offer(bn, v, j);
                 }
-                unsigned m = __ballot_sync(0xffffffffu, cand);
+                unsigned m = __ballot_sync(0xffffffffu, cand && d_is_interval(v));
                 while (m) {
                     const int src = __ffs(m) - 1;
                     m &= m - 1;
@@ -666,10 +688,26 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                         drow[jj] = d;
                         D[(size_t)jj * Rp + i] = d;
                     }
-                    if (ajj) rb_offer(ba, d, jj);
-                    else rb_offer(bn, d, jj);
+                    if (lane == src) {
+                        if (ajj) rb_offer(ba, d, jj);
+                        else rb_offer(bn, d, jj);
+                    }
                 }
             }
+        }
+        ba = warp_min_rb(ba);
+        bn = warp_min_rb(bn);
+        // the single candidate (if any) sits in exactly one lane
+        const unsigned oa = __ballot_sync(0xffffffffu, sa.j != kNoJ), on = __ballot_sync(0xffffffffu, sn.j != kNoJ);
+        if (na == 1 && oa) {
+            const int src = __ffs(oa) - 1;
+            ba.d = __shfl_sync(0xffffffffu, sa.d, src);
+            ba.j = __shfl_sync(0xffffffffu, sa.j, src);
+        }
+        if (nbn == 1 && on) {
+            const int src = __ffs(on) - 1;
+            bn.d = __shfl_sync(0xffffffffu, sn.d, src);
+            bn.j = __shfl_sync(0xffffffffu, sn.j, src);
         }
         if (lane == 0) {
             const int r = i - lo;
@@ -899,15 +937,81 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         // read from it.
         // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
         Pair ca = pair_none(), cn = pair_none();
-        for (int i = lo + tid; i < hi; i += kThreads) {
-            if (cnt[i] == 0u || i == a_prev) continue;
-            const int r = i - lo;
-            if (bAj[r] >= 0) pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
-            if (SPEC && bNj[r] >= 0) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
+        if (F32) {
+            // row caches may hold intervals: the stage minimum is among the rows whose
+            // lower bound reaches below the smallest upper bound; those are made
+            // exact (warps), then the usual lexicographic (d, min id, max id) pick
+            if (tid == 0) {
+                if (a_prev >= 0) {
+                    const int r = a_prev - lo;
+                    bAd[r] = rpart[0].d;
+                    bAj[r] = rpart[0].j == kNoJ ? -1 : rpart[0].j;
+                    bNd[r] = rpart[1].d;
+                    bNj[r] = rpart[1].j == kNoJ ? -1 : rpart[1].j;
+                }
+                ninv = 0;
+                sScan = 0;
+            }
+            __syncthreads();
+            double uA = kInf, uN = kInf;
+            for (int i = lo + tid; i < hi; i += kThreads) {
+                if (cnt[i] == 0u) continue;
+                const int r = i - lo;
+                double l2, h2;
+                if (bAj[r] >= 0) { d_unpack(bAd[r], l2, h2); uA = fmin(uA, h2); }
+                if (bNj[r] >= 0) { d_unpack(bNd[r], l2, h2); uN = fmin(uN, h2); }
+            }
+            uA = block_min_rb(RowBest{uA, 0}, rscr).d;
+            uN = block_min_rb(RowBest{uN, 0}, rscr).d;
+            unsigned short* clist = reinterpret_cast<unsigned short*>(inv);
+            for (int i = lo + tid; i < hi; i += kThreads) {
+                if (cnt[i] == 0u) continue;
+                const int r = i - lo;
+                double l2, h2;
+                if (bAj[r] >= 0) {
+                    d_unpack(bAd[r], l2, h2);
+                    if (l2 <= uA) clist[atomicAdd(&sScan, 1)] = (unsigned short)i;
+                }
+                if (bNj[r] >= 0) {
+                    d_unpack(bNd[r], l2, h2);
+                    if (l2 <= uN) clist[atomicAdd(&sScan, 1)] = (unsigned short)(i | 0x4000);
+                }
+            }
+            __syncthreads();
+            const int nc = sScan;
+            for (int t = warp; t < nc; t += kWarps) {
+                const int e = clist[t], i = e & 0x3fff, st = e >> 14, r = i - lo;
+                const int j = st ? bNj[r] : bAj[r];
+                const double v = st ? bNd[r] : bAd[r];
+                if (!d_is_interval(v)) continue;
+                const double d = warp_exact<M>(nullptr, sums + (size_t)i * B, (double)cnt[i], sums + (size_t)j * B,
+                                               (double)cnt[j], B, lane);
+                if (lane == 0) {
+                    if (st) bNd[r] = d;
+                    else bAd[r] = d;
+                    D[(size_t)i * Rp + j] = d;
+                    D[(size_t)j * Rp + i] = d;
+                }
+            }
+            __syncthreads();
+            for (int t = tid; t < nc; t += kThreads) {
+                const int e = clist[t], i = e & 0x3fff, r = i - lo;
+                if (e >> 14) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
+                else pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
+            }
+            ca = block_min_pair(ca, pscr);
+            cn = block_min_pair(cn, pscr);
+        } else {
+            for (int i = lo + tid; i < hi; i += kThreads) {
+                if (cnt[i] == 0u || i == a_prev) continue;
+                const int r = i - lo;
+                if (bAj[r] >= 0) pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
+                if (SPEC && bNj[r] >= 0) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
+            }
+            if (tid == 0) ninv = 0;
+            ca = block_min_pair(ca, pscr);
+            if (SPEC) cn = block_min_pair(cn, pscr);
         }
-        if (tid == 0) ninv = 0;
-        ca = block_min_pair(ca, pscr);
-        if (SPEC) cn = block_min_pair(cn, pscr);
         if (tid == 0) {
             slot[par].selA = ca;
             slot[par].selN = cn;
@@ -942,7 +1046,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 rb_offer(PN, s.rpN.d, s.rpN.j);
             }
         }
-        if (a_prev >= 0) {
+        if (a_prev >= 0 && !F32) {  // (F32: a_prev's row joined the candidates above)
             if (PA.j != kNoJ) pair_offer(A, make_pair(PA.d, a_prev, PA.j));
             if (SPEC && PN.j != kNoJ) pair_offer(N, make_pair(PN.d, a_prev, PN.j));
             if (tid == 0 && a_prev >= lo && a_prev < hi) {
@@ -1249,9 +1353,11 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             ss.issued += max(0, ss.nst - kStages);
 #endif
             if (F32) {
-                // intervals around every d(a, j); exact re-evaluation only where an
-                // interval cannot settle a comparison: row j's cached best, or a's
-                // own minimum (any column whose dlo reaches below min dhi)
+                // an interval around every d(a, j) goes to D; offers compare
+                // intervals and only an overlap with row j's cached best is resolved
+                // exactly. a's own best: the columns whose lower bound reaches below
+                // the stage's smallest upper bound -- one is kept as an interval,
+                // several are made exact.
                 const double* xn = bt.xnorm + (size_t)sec * Rp;
                 double dlo[NQ], dhi[NQ];
                 double uA = kInf, uN = kInf;
@@ -1265,41 +1371,81 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                         else uN = fmin(uN, dhi[q]);
                     }
                 }
-                {
-                    RowBest ra2 = block_min_rb(RowBest{uA, 0}, rscr);
-                    RowBest rn2 = block_min_rb(RowBest{uN, 0}, rscr);
-                    uA = ra2.d;
-                    uN = rn2.d;
-                }
+                int* cntF = misc + 10;  // [0] overlaps, [1] a-candidates adjacent, [2] non-adjacent
+                if (tid == 0) { cntF[0] = 0; cntF[1] = 0; cntF[2] = 0; }
+                uA = block_min_rb(RowBest{uA, 0}, rscr).d;
+                uN = block_min_rb(RowBest{uN, 0}, rscr).d;
+                unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);  // overlaps
+                unsigned short* l2 = l1 + Rs;                                 // a's candidates
+                // (l1 and l2 each hold at most one entry per own column)
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
                     if (!valid[q]) continue;
                     const int j = jq[q], r = j - lo;
-                    const double bd = isadj[q] ? bAd[r] : bNd[r];
-                    if (dlo[q] <= bd || dlo[q] <= (isadj[q] ? uA : uN)) {
-                        inv[atomicAdd(&sScan, 1)] = (j << 1) | (isadj[q] ? 1 : 0);
+                    const bool aj = isadj[q];
+                    const unsigned short e = (unsigned short)(j | (aj ? 0 : 0x4000));
+                    const double v = d_pack_interval(dlo[q], dhi[q]);
+                    D[(size_t)j * Rp + a] = v;
+                    D[(size_t)a * Rp + j] = v;
+                    if (dlo[q] <= (aj ? uA : uN)) {
+                        l2[atomicAdd(&sScan, 1)] = e;
+                        atomicAdd(&cntF[aj ? 1 : 2], 1);
+                    }
+                    double& bv = aj ? bAd[r] : bNd[r];
+                    int& bj = aj ? bAj[r] : bNj[r];
+                    if (bj < 0) {
+                        bv = v;
+                        bj = a;
                     } else {
-                        const double v = d_pack_interval(dlo[q], dhi[q]);
-                        D[(size_t)j * Rp + a] = v;
-                        D[(size_t)a * Rp + j] = v;
+                        double bl, bh;
+                        d_unpack(bv, bl, bh);
+                        if (dhi[q] < bl) { bv = v; bj = a; }
+                        else if (!(dlo[q] > bh)) l1[atomicAdd(&cntF[0], 1)] = e;
                     }
                 }
                 __syncthreads();
-                const int nex = sScan;
-                for (int t = warp; t < nex; t += kWarps) {
-                    const int j = inv[t] >> 1;
-                    const bool adjj = inv[t] & 1;
-                    const double d = warp_exact<M>(mua, nullptr, nn, sums + (size_t)j * B, (double)cnt[j], B, lane);
+                const int n1 = cntF[0], n2 = sScan, nA = cntF[1], nN = cntF[2];
+                // overlaps with row j's cached best: exact d(a, j) and exact best
+                for (int t = warp; t < n1; t += kWarps) {
+                    const int e = l1[t], j = e & 0x3fff, r = j - lo;
+                    const bool aj = !(e >> 14);
+                    const double* sj = sums + (size_t)j * B;
+                    const double cj = (double)cnt[j];
+                    const double daj = warp_exact<M>(mua, nullptr, nn, sj, cj, B, lane);
+                    const int bj = aj ? bAj[r] : bNj[r];
+                    double db = aj ? bAd[r] : bNd[r];
+                    const bool binterval = d_is_interval(db);
+                    if (binterval) db = warp_exact<M>(nullptr, sj, cj, sums + (size_t)bj * B, (double)cnt[bj], B, lane);
                     if (lane == 0) {
-                        D[(size_t)j * Rp + a] = d;
-                        D[(size_t)a * Rp + j] = d;
-                        const int r = j - lo;
-                        if (adjj) {
-                            rb_offer(pA, d, j);
-                            cache_offer(bAd[r], bAj[r], d, a);
-                        } else {
-                            rb_offer(pN, d, j);
-                            cache_offer(bNd[r], bNj[r], d, a);
+                        D[(size_t)j * Rp + a] = daj;
+                        D[(size_t)a * Rp + j] = daj;
+                        if (binterval) {
+                            D[(size_t)j * Rp + bj] = db;
+                            D[(size_t)bj * Rp + j] = db;
+                        }
+                        const bool take_a = daj < db || (daj == db && a < bj);
+                        if (aj) { bAd[r] = take_a ? daj : db; bAj[r] = take_a ? a : bj; }
+                        else { bNd[r] = take_a ? daj : db; bNj[r] = take_a ? a : bj; }
+                    }
+                }
+                __syncthreads();
+                // a's best per stage
+                for (int t = warp; t < n2; t += kWarps) {
+                    const int e = l2[t], j = e & 0x3fff;
+                    const bool aj = !(e >> 14);
+                    if ((aj ? nA : nN) == 1) {
+                        if (lane == 0) {
+                            const RowBest c{D[(size_t)a * Rp + j], j};
+                            if (aj) pA = c;
+                            else pN = c;
+                        }
+                    } else {
+                        const double d = warp_exact<M>(mua, nullptr, nn, sums + (size_t)j * B, (double)cnt[j], B, lane);
+                        if (lane == 0) {
+                            D[(size_t)j * Rp + a] = d;
+                            D[(size_t)a * Rp + j] = d;
+                            if (aj) rb_offer(pA, d, j);
+                            else rb_offer(pN, d, j);
                         }
                     }
                 }
