@@ -390,17 +390,28 @@ __device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
 template <int M>
 __device__ __forceinline__ double warp_exact(const double* mi_smem, const double* si, double ci, const double* sj,
                                              double cj, int B, int lane) {
+    // the per-band terms are independent (all lanes in parallel); only the
+    // ascending-band sum is a serial chain, fed by shuffles issued ahead of it
     double s = 0.0;
     for (int k0 = 0; k0 < B; k0 += 32) {
         const int k = k0 + lane;
-        double vi = 0.0, vj = 0.0;
+        double term = 0.0;
         if (k < B) {
-            vi = mi_smem ? mi_smem[k] : __ddiv_rn(si[k], ci);
-            vj = __ddiv_rn(sj[k], cj);
+            const double vi = mi_smem ? mi_smem[k] : __ddiv_rn(si[k], ci);
+            const double vj = __ddiv_rn(sj[k], cj);
+            if (M == kSam) {
+                term = __dmul_rn(vi, vj);
+            } else {
+                const double t = __dsub_rn(vi, vj);
+                term = __dmul_rn(t, t);
+            }
         }
         const int kn = min(32, B - k0);
-        for (int kk = 0; kk < kn; ++kk)
-            s = acc_step<M>(s, __shfl_sync(0xffffffffu, vi, kk), __shfl_sync(0xffffffffu, vj, kk));
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) {
+            const double tk = __shfl_sync(0xffffffffu, term, kk);
+            if (kk < kn) s = __dadd_rn(s, tk);
+        }
     }
     return pair_finish<M>(ci, cj, s, 0.0, 0.0);
 }
@@ -592,15 +603,28 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     };
 
     // F32 rescan: D rows hold exact values and intervals; the row's best may be
-    // cached as an interval. Pass 1: per stage the smallest upper bound U (and
-    // the entry holding it); pass 2: entries with lower bound <= U are the only
-    // possible minima -- one such entry is cached as it is, several are resolved
-    // exactly (intervals evaluated by the warp, written back to D).
+    // cached as an interval. One pass finds, per stage, the smallest upper bound U
+    // and the two smallest lower bounds: if the second lies above U the entry with
+    // the smallest lower bound is the row's minimum (cached as it is); otherwise a
+    // second pass takes the exact lexicographic minimum of every entry whose
+    // lower bound reaches U (intervals evaluated by the warp, written back to D).
+    struct Lo2 {
+        double l1, v1, l2, u;
+        int j1;
+    };
+    auto lo2_put = [](Lo2& x, double l, int j, double v) {
+        if (l < x.l1 || (l == x.l1 && j < x.j1)) {
+            x.l2 = x.l1;
+            x.l1 = l; x.j1 = j; x.v1 = v;
+        } else if (l < x.l2) {
+            x.l2 = l;
+        }
+    };
     auto rescanf = [&](int i, int mask, int ex) {
         const uint32_t* arow = adj + (size_t)i * W;
         double* drow = D + (size_t)i * Rp;
         const bool live_i = cnt[i] != 0u;
-        double uA = kInf, uN = kInf;  // min upper bound per stage
+        Lo2 xa{kInf, kInf, kInf, kInf, kNoJ}, xn{kInf, kInf, kInf, kInf, kNoJ};
         constexpr int U = 16;
         if (live_i) {
             for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
@@ -621,58 +645,46 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     if (aj ? !(mask & 1) : !(mask & 2)) continue;
                     double lo2, hi2;
                     d_unpack(dv[u], lo2, hi2);
-                    if (aj) uA = fmin(uA, hi2);
-                    else uN = fmin(uN, hi2);
+                    Lo2& x = aj ? xa : xn;
+                    x.u = fmin(x.u, hi2);
+                    lo2_put(x, lo2, j, dv[u]);
                 }
             }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            uA = fmin(uA, __shfl_xor_sync(0xffffffffu, uA, o));
-            uN = fmin(uN, __shfl_xor_sync(0xffffffffu, uN, o));
-        }
-        // pass 2: candidates (lo <= U). A stage with one candidate caches it as it
-        // is; a stage with several takes their exact lexicographic minimum
-        // (intervals evaluated by the warp and written back to D).
-        RowBest ba = rb_none(), bn = rb_none();   // exact minima
-        RowBest sa = rb_none(), sn = rb_none();   // the single candidate (packed value, j)
-        int na = 0, nbn = 0;
-        auto candidate = [&](int j, bool& aj, double& v) {
-            aj = false;
-            v = kInf;
-            if (j < 0 || j == i || j == ex || cnt[j] == 0u) return false;
-            aj = (arow[j >> 5] >> (j & 31)) & 1u;
-            if (aj ? !(mask & 1) : !(mask & 2)) return false;
-            v = __ldcs(drow + j);
-            double lo2, hi2;
-            d_unpack(v, lo2, hi2);
-            return lo2 <= (aj ? uA : uN);
-        };
-        if (live_i && (uA < kInf || uN < kInf)) {
-            for (int s0 = 0; s0 < ss.S; s0 += 32) {
-                const int sl = s0 + lane;
-                bool aj;
-                double v;
-                const int j = sl < ss.S ? col[sl] : -1;
-                const bool cand = candidate(j, aj, v);
-                na += __popc(__ballot_sync(0xffffffffu, cand && aj));
-                nbn += __popc(__ballot_sync(0xffffffffu, cand && !aj));
-                if (cand) {
-                    if (aj) sa = RowBest{v, j};
-                    else sn = RowBest{v, j};
-                }
+#pragma unroll
+            for (int st = 0; st < 2; ++st) {
+                Lo2& x = st ? xn : xa;
+                const double l1 = __shfl_xor_sync(0xffffffffu, x.l1, o), v1 = __shfl_xor_sync(0xffffffffu, x.v1, o);
+                const double l2 = __shfl_xor_sync(0xffffffffu, x.l2, o), u2 = __shfl_xor_sync(0xffffffffu, x.u, o);
+                const int j1 = __shfl_xor_sync(0xffffffffu, x.j1, o);
+                x.u = fmin(x.u, u2);
+                if (j1 != kNoJ) lo2_put(x, l1, j1, v1);
+                if (l2 < x.l2) x.l2 = l2;
             }
         }
-        if (na > 1 || nbn > 1) {
+        RowBest ba{xa.v1, xa.j1}, bn{xn.v1, xn.j1};  // single candidate (or none)
+        const bool multA = xa.j1 != kNoJ && xa.l2 <= xa.u, multN = xn.j1 != kNoJ && xn.l2 <= xn.u;
+        if (live_i && (multA || multN)) {
+            if (multA) ba = rb_none();
+            if (multN) bn = rb_none();
             const double* si = sums + (size_t)i * B;
             const double ci = (double)cnt[i];
             for (int s0 = 0; s0 < ss.S; s0 += 32) {
                 const int sl = s0 + lane;
-                bool aj;
-                double v;
                 const int j = sl < ss.S ? col[sl] : -1;
-                bool cand = candidate(j, aj, v);
-                cand = cand && (aj ? na > 1 : nbn > 1);
+                bool cand = false, aj = false;
+                double v = kInf;
+                if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                    aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                    if (aj ? (mask & 1) && multA : (mask & 2) && multN) {
+                        v = __ldcs(drow + j);
+                        double lo2, hi2;
+                        d_unpack(v, lo2, hi2);
+                        cand = lo2 <= (aj ? xa.u : xn.u);
+                    }
+                }
                 if (cand && !d_is_interval(v)) {
                     if (aj) rb_offer(ba, v, j);
                     else rb_offer(bn, v, j);
@@ -694,20 +706,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     }
                 }
             }
-        }
-        ba = warp_min_rb(ba);
-        bn = warp_min_rb(bn);
-        // the single candidate (if any) sits in exactly one lane
-        const unsigned oa = __ballot_sync(0xffffffffu, sa.j != kNoJ), on = __ballot_sync(0xffffffffu, sn.j != kNoJ);
-        if (na == 1 && oa) {
-            const int src = __ffs(oa) - 1;
-            ba.d = __shfl_sync(0xffffffffu, sa.d, src);
-            ba.j = __shfl_sync(0xffffffffu, sa.j, src);
-        }
-        if (nbn == 1 && on) {
-            const int src = __ffs(on) - 1;
-            bn.d = __shfl_sync(0xffffffffu, sn.d, src);
-            bn.j = __shfl_sync(0xffffffffu, sn.j, src);
+            if (multA) ba = warp_min_rb(ba);
+            if (multN) bn = warp_min_rb(bn);
         }
         if (lane == 0) {
             const int r = i - lo;
