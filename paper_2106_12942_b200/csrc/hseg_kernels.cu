@@ -180,7 +180,12 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
 // per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
 #ifndef RHSEG_F32FILTER
-#define RHSEG_F32FILTER 1  // stream fp32 filter means (exact fp64 re-evaluation) when w > 0
+// Experimental (off): stream fp32 filter means with exact fp64 re-evaluation.
+// Bit-exact (the GPU suite passes with it on) but slower on C4 (loop 1028 vs
+// 877 ms): the exact re-evaluations it needs every step (argmin winners, offer
+// overlaps, multi-candidate rescans) sit on each CTA's serial step chain and
+// cost more than the halved stream saves. profiles/r01_loop_variants.md.
+#define RHSEG_F32FILTER 0
 #endif
 #if defined(RHSEG_DIRECT) && RHSEG_DIRECT
 #undef RHSEG_F32FILTER
