@@ -191,6 +191,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #undef RHSEG_F32FILTER
 #define RHSEG_F32FILTER 0  // the unstaged experiment streams fp64 only
 #endif
+#ifndef RHSEG_COMPACT_K
+#define RHSEG_COMPACT_K 16  // compaction threshold: holes^2 >= K * S (K=16: C4 loop 874 -> 864 ms)
+#endif
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -848,7 +851,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // Geometry of the next step's stream + its first kStages band chunks in flight
     // (compacting first when >= 25% of the own columns are holes).
     auto begin_stream = [&]() {
-        if (ss.S >= 64 && 4 * ss.holes >= ss.S) compact();
+        // compact when holes >= 2 sqrt(S): balances the streamed holes (~1/sqrt(S) of
+        // the bytes) against the copy cost (2 S B words every 2 sqrt(S) merges)
+        if (ss.S >= 64 && ss.holes * ss.holes >= RHSEG_COMPACT_K * ss.S) compact();
         constexpr int kAlign = 16 / ES;  // bulk copies move multiples of 16 bytes
         ss.S2 = (ss.S + kAlign - 1) / kAlign * kAlign;
         ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * ES))) : B;
