@@ -159,6 +159,21 @@ int rhseg_scan_nonadjacent(int64_t row_start, int64_t row_stop, int64_t col_tile
                            const int64_t *indptr, const int64_t *indices, double *out_d,
                            int64_t *out_j);
 
+/* ---- output files at scale (cli.py:386-390, hsio.py:85-101, manifest.py:22-27) ---- */
+/* Python repr of a double (shortest round trip, repr layout; json.dumps spelling of
+ * inf/nan) into buf (cap >= 32). Host-only, no device needed. */
+int rhseg_format_float(double x, char *buf, int32_t cap);
+/* sha256 of n bytes as 64 hex chars + NUL (hex65). Host-only. */
+int rhseg_sha256_hex(const void *data, int64_t n, char *hex65);
+/* Labels PGM + merge-log JSONL byte-identical to the reference CLI's files, from
+ * host arrays (rhseg_result_sections / _log / _labels); content_hash_hex65 =
+ * sha256(pgm || jsonl) = the reference manifest's content_hash. Host-only. */
+int rhseg_write_outputs_host(const char *pgm_path, const char *jsonl_path, int32_t width, int32_t height,
+                             const int32_t *labels, int32_t n_sections, const int32_t *sec_level,
+                             const int32_t *sec_row, const int32_t *sec_col, const int64_t *sec_count,
+                             const int32_t *survivor, const int32_t *absorbed, const double *dissim,
+                             const uint8_t *kind, char *content_hash_hex65, int64_t *jsonl_bytes);
+
 /* ---- measurement helpers ------------------------------------------------------ */
 /* Per-kernel device time of the last run: [0] leaf/graph init, [1] all-pairs D init,
  * [2] merge loops, [3] stitch+resolve+labels (ms, CUDA events on the run stream). */

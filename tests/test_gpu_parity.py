@@ -278,3 +278,19 @@ def test_extension_measures_hseg_run_and_step(measure, oracle):
     first = rh.hseg_step(g2, rh.HsegParams(0.5, 3, measure))
     assert (first.survivor_id, first.absorbed_id, first.dissimilarity) == (
         h.records[0].survivor_id, h.records[0].absorbed_id, h.records[0].dissimilarity)
+
+
+@pytest.mark.parametrize("name", ["c1_64x64x32", "crit2_64x64x16_L3", "c2_144x144x220_L3"])
+def test_native_outputs_hash_equals_reference(name, tmp_path):
+    """End to end: the device run's merge-log JSONL written natively has the sha256
+    of the reference CLI's JSONL for the same cube (cli.py:387-390)."""
+    import hashlib
+
+    from paper_2106_12942_b200 import outputs
+
+    z = load(name + ".npz")
+    spec, levels, w, t, st = SYNTH[name]
+    res = rh.rhseg_run(synth_image(spec), rh.RhsegParams(rh.HsegParams(w, t), levels, st))
+    out = outputs.write_outputs(res, tmp_path / "o.pgm", tmp_path / "o.merges.jsonl")
+    assert hashlib.sha256((tmp_path / "o.merges.jsonl").read_bytes()).hexdigest() == str(z["jsonl_sha256"])
+    assert len(out["content_hash"]) == 64
