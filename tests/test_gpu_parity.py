@@ -294,3 +294,32 @@ def test_native_outputs_hash_equals_reference(name, tmp_path):
     out = outputs.write_outputs(res, tmp_path / "o.pgm", tmp_path / "o.merges.jsonl")
     assert hashlib.sha256((tmp_path / "o.merges.jsonl").read_bytes()).hexdigest() == str(z["jsonl_sha256"])
     assert len(out["content_hash"]) == 64
+
+
+def test_largest_section_first_merges_vs_oracle(oracle):
+    """The largest supported section (128x128 = 16384 regions: 16-CTA cluster,
+    1024 rows per CTA, 2 GB D): the first merges against the oracle."""
+    img, _ = rh.gen_synthetic(128, 6, 4, 6, 3.0, 11)
+    R0 = 128 * 128
+    for w in (0.21, 0.0):
+        g = rh.init_region_graph(img, 8)
+        h = rh.hseg_run(g, rh.HsegParams(w, R0 - 4))
+        oracle.set_threads(os.cpu_count() or 1)
+        ref = oracle.rhseg_run(img.samples, 1, w, R0 - 4)
+        assert [(r.survivor_id, r.absorbed_id) for r in h.records] == list(
+            zip(ref["log_survivor"].tolist(), ref["log_absorbed"].tolist()))
+        got = np.array([r.dissimilarity for r in h.records])
+        assert np.array_equal(got.view(np.uint64), ref["log_dissim"].view(np.uint64))
+
+
+@pytest.mark.parametrize("bands,conn", [(1, 4), (300, 8), (37, 4)])
+def test_band_counts_and_connectivity_vs_oracle(bands, conn, oracle):
+    rng = np.random.default_rng(bands)
+    s = rng.normal(50, 20, size=(bands, 24, 24)).astype(np.float32)
+    img = rh.HyperImage(24, 24, bands, s)
+    for w in (0.0, 0.5):
+        res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(w, 5), 2, 11),
+                           executor=rh.B200Executor(connectivity=conn))
+        ref = oracle.rhseg_run(s, 2, w, 5, 11, connectivity=conn)
+        assert_log_equal(_flat(res), ref, f"B={bands} conn={conn} w={w}")
+        assert np.array_equal(res.labels.labels, ref["labels"])
