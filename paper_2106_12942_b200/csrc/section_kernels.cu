@@ -141,7 +141,11 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
     __shared__ int scratch[kWarps];
     int cidx[4];
     for (int k = 0; k < 4; ++k) cidx[k] = (2 * pr + (k >> 1)) * ccols + (2 * pc + (k & 1));
-    // 1. dense renumber maps
+    // 1. dense renumber maps; the parent's `parent` array doubles as the inverse
+    //    list (parent id -> child k, child id) until step 5 resets it
+    uint32_t* pcnt = pa.count + (size_t)P * pa.Rp;
+    int* pparent = pa.parent + (size_t)P * pa.Rp;
+    double* pmu = pa.mu + P * pa.mu_stride();
     int base = 0;
     for (int k = 0; k < 4; ++k) {
         const int c = cidx[k];
@@ -154,46 +158,35 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
             int tot;
             const int pre = block_excl_scan(live, scratch, tot);
             if (i < R0c) map[i] = live ? base + pre : -1;
+            if (live) pparent[base + pre] = (k << 16) | i;
             base += tot;
         }
     }
     __syncthreads();
-    // 2. counts, sums (all parent copies), mu, adjacency
-    uint32_t* pcnt = pa.count + (size_t)P * pa.Rp;
-    int* pparent = pa.parent + (size_t)P * pa.Rp;
-    double* pmu = pa.mu + P * pa.mu_stride();
-    for (int i = threadIdx.x; i < pa.Rp; i += kThreads) pparent[i] = -1;
-    for (int k = 0; k < 4; ++k) {
-        const int c = cidx[k];
-        const int R0c = ch.R0[c];
-        const uint32_t* ccnt = ch.count + (size_t)c * ch.Rp;
+    // 2. counts, sums (all parent copies), mu, adjacency -- live regions only
+    const int R = base;  // == pa.R0[P]
+    for (int idx = threadIdx.x; idx < R * B; idx += kThreads) {
+        const int m = idx / B, q = idx - m * B;
+        const int src = pparent[m], k = src >> 16, i = src & 0xffff, c = cidx[k];
+        const double cn = (double)ch.count[(size_t)c * ch.Rp + i];
+        if (q == 0) pcnt[m] = ch.count[(size_t)c * ch.Rp + i];
+        const double s = ch.sums[(size_t)c * ch.C * ch.sums_copy() + (size_t)i * B + q];  // copy 0
+        for (int cc = 0; cc < pa.C; ++cc)
+            pa.sums[((size_t)P * pa.C + cc) * pa.sums_copy() + (size_t)m * B + q] = s;
+        pmu[(size_t)q * pa.Rp + m] = __ddiv_rn(s, cn);
+    }
+    for (int idx = threadIdx.x; idx < R * ch.W; idx += kThreads) {
+        const int m = idx / ch.W, w = idx - m * ch.W;
+        const int src = pparent[m], k = src >> 16, i = src & 0xffff, c = cidx[k];
+        uint32_t bits = ch.adj[(size_t)c * ch.C * ch.adj_copy() + (size_t)i * ch.W + w];  // copy 0
         const int* map = cmap + (size_t)c * ch.Rp;
-        const double* csums = ch.sums + (size_t)c * ch.C * ch.sums_copy();  // copy 0
-        const uint32_t* cadj = ch.adj + (size_t)c * ch.C * ch.adj_copy();   // copy 0
-        for (int i = threadIdx.x; i < R0c; i += kThreads)
-            if (ccnt[i] != 0u) pcnt[map[i]] = ccnt[i];
-        for (int idx = threadIdx.x; idx < R0c * B; idx += kThreads) {
-            const int i = idx / B, q = idx - i * B;
-            if (ccnt[i] == 0u) continue;
-            const int m = map[i];
-            const double s = csums[(size_t)i * B + q];
+        while (bits) {
+            const int j = (w << 5) + __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int mj = map[j];
             for (int cc = 0; cc < pa.C; ++cc)
-                pa.sums[((size_t)P * pa.C + cc) * pa.sums_copy() + (size_t)m * B + q] = s;
-            pmu[(size_t)q * pa.Rp + m] = __ddiv_rn(s, (double)ccnt[i]);
-        }
-        for (int idx = threadIdx.x; idx < R0c * ch.W; idx += kThreads) {
-            const int i = idx / ch.W, w = idx - i * ch.W;
-            if (ccnt[i] == 0u) continue;
-            uint32_t bits = cadj[(size_t)i * ch.W + w];
-            const int m = map[i];
-            while (bits) {
-                const int j = (w << 5) + __ffs(bits) - 1;
-                bits &= bits - 1;
-                const int mj = map[j];
-                for (int cc = 0; cc < pa.C; ++cc)
-                    atomicOr(&pa.adj[((size_t)P * pa.C + cc) * pa.adj_copy() + (size_t)m * pa.W + (mj >> 5)],
-                             1u << (mj & 31));
-            }
+                atomicOr(&pa.adj[((size_t)P * pa.C + cc) * pa.adj_copy() + (size_t)m * pa.W + (mj >> 5)],
+                         1u << (mj & 31));
         }
     }
     if (pa.measure == kSam) {
@@ -234,7 +227,11 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
             link(e - 1, r + 1, e, r);
         }
     }
+    // 5. union-find links start empty (the inverse list lived here)
+    __syncthreads();
+    for (int i = threadIdx.x; i < pa.Rp; i += kThreads) pparent[i] = -1;
 }
+
 
 void launch_stitch(const SectionBatch& child, int child_cols, const SectionBatch& parent, int parent_cols,
                    int* child_map, int connectivity, cudaStream_t st) {
