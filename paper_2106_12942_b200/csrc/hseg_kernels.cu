@@ -1092,6 +1092,29 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
 
         mark(1);
+        // (C1) rows whose cached partner was a or b (rescanned in C2, after the
+        // merge); their D rows are prefetched into L2 while the merge runs
+        for (int i = lo + tid; i < hi; i += kThreads) {
+            if (cnt[i] == 0u || i == a || i == b) continue;
+            const int r = i - lo;
+            int mask = 0;
+            if (TOP2) {
+                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], a);
+                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], b);
+                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], a);
+                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], b);
+                if (bAj[r] < 0 && !(cx[r] & 1)) mask |= 1;
+                if (bNj[r] < 0 && !(cx[r] & 2)) mask |= 2;
+            } else {
+                if (bAj[r] == a || bAj[r] == b) mask |= 1;
+                if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
+            }
+            if (mask) {
+                inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
+                // its D row is read by the rescan after the merge: start the fetch now
+                bulk_prefetch_l2(D + (size_t)i * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
+            }
+        }
         // (C) merge (graph.py:229-264) on this CTA's private copies
         const double nn = __dadd_rn((double)cnt[a], (double)cnt[b]);
         const bool own_a = a >= lo && a < hi;
@@ -1172,23 +1195,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         // skipping a (its entries are refreshed by the row-a pass, which then
         // offers (d(i, a), a) to every row) and b (dead). Their D loads overlap the
         // row-a stream already in flight.
-        for (int i = lo + tid; i < hi; i += kThreads) {
-            if (cnt[i] == 0u || i == a) continue;
-            const int r = i - lo;
-            int mask = 0;
-            if (TOP2) {
-                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], a);
-                l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], b);
-                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], a);
-                l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], b);
-                if (bAj[r] < 0 && !(cx[r] & 1)) mask |= 1;
-                if (bNj[r] < 0 && !(cx[r] & 2)) mask |= 2;
-            } else {
-                if (bAj[r] == a || bAj[r] == b) mask |= 1;
-                if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
-            }
-            if (mask) inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
-        }
         __syncthreads();
         {
             const int ni = ninv;
