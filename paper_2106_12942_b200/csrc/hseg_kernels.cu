@@ -229,7 +229,8 @@ struct LoopSmem {
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
-__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2, bool f32) {
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2, bool f32,
+                                                     int stage_bytes) {
     const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
     size_t o = 0;
@@ -259,7 +260,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.cx = o;    o = align16(o + (top2 ? Rs : 0));
     o = (o + 127) & ~size_t(127);
     L.ring = o;
-    o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * (top2 ? kStageBytesTop2 : kStageBytes) + kThreads * 8 : 0;
+    o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * stage_bytes + kThreads * 8 : 0;
     L.total = o;
     return L;
 }
@@ -267,8 +268,12 @@ __host__ __device__ inline bool use_top2(bool spec, int C, int measure) { return
 __host__ __device__ inline bool use_f32(bool spec, int C, int measure) {
     return RHSEG_F32FILTER && spec && C == 1 && measure != kSam;
 }
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure) {
-    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure)).total;
+int hseg_loop_stage_bytes(bool spec, int C, int measure) {
+    return use_top2(spec, C, measure) ? kStageBytesTop2 : kStageBytes;
+}
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes) {
+    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure), stage_bytes)
+        .total;
 }
 bool hseg_use_f32(bool spec, int C, int measure) { return use_f32(spec, C, measure); }
 int hseg_loop_max_rows() { return kMaxSlots; }
@@ -486,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     constexpr bool F32 = RHSEG_F32FILTER && SPEC && !CLUSTER && M != kSam;
     using SE = typename std::conditional<F32, float, double>::type;  // streamed element
     constexpr int ES = (int)sizeof(SE);
-    constexpr int SB = TOP2 ? kStageBytesTop2 : kStageBytes;
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32);
+    const int SB = bt.stage_bytes;  // ring stage size chosen by the host (occupancy-aware)
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32, SB);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -1543,7 +1548,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
-    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure);
+    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure, b.stage_bytes);
     void (*kern)(SectionBatch);
 #define RHSEG_PICK(M)                                                                              \
     if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true, M> : hseg_loop_kernel<true, false, M>; \

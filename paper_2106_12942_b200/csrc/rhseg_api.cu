@@ -219,12 +219,23 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
     const bool spec = weight > 0.0;
     auto fits = [&](int C) {
-        return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure) <= 220 * 1024 &&
+        return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure, hseg_loop_stage_bytes(spec, C, lv.measure)) <=
+                   220 * 1024 &&
                (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
     };
     // grow the cluster until the per-CTA row slice fits shared memory
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
     if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
+    // stream ring: the default keeps two CTAs per SM; when the level has at most one
+    // CTA per SM anyway, a bigger ring keeps more of each CTA's stream in flight
+    int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
+    if (spec && (long long)lv.nsec * lv.C <= c->nsm) {
+        for (int sb = 96 * 1024; sb > stage_bytes; sb -= 8 * 1024)
+            if (hseg_loop_smem(lv.Rp, lv.C, lv.B, spec, lv.measure, sb) <= 220 * 1024) {
+                stage_bytes = sb;
+                break;
+            }
+    }
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
@@ -270,6 +281,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.edge = lv.edge;
     b.npx = (int)npx;
     b.spec = spec ? 1 : 0;
+    b.stage_bytes = stage_bytes;
     b.measure = lv.measure;
     b.nrm2 = lv.measure == 2 ? reinterpret_cast<double*>(K + oN2) : nullptr;
     b.weight = weight;
