@@ -194,6 +194,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #ifndef RHSEG_COMPACT_K
 #define RHSEG_COMPACT_K 16  // compaction threshold: holes^2 >= K * S (K=16: C4 loop 874 -> 864 ms)
 #endif
+#ifndef RHSEG_RESCAN_PREFETCH
+#define RHSEG_RESCAN_PREFETCH 1
+#endif
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -1098,7 +1101,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 
         mark(1);
         // (C1) rows whose cached partner was a or b (rescanned in C2, after the
-        // merge); their D rows are prefetched into L2 while the merge runs
+        // merge); their D rows are prefetched into L2 while the merge runs.
+        // The barrier publishes thread 0's update of a_prev's caches (above).
+        __syncthreads();
         for (int i = lo + tid; i < hi; i += kThreads) {
             if (cnt[i] == 0u || i == a || i == b) continue;
             const int r = i - lo;
@@ -1117,7 +1122,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (mask) {
                 inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
                 // its D row is read by the rescan after the merge: start the fetch now
-                bulk_prefetch_l2(D + (size_t)i * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
+                if (RHSEG_RESCAN_PREFETCH) bulk_prefetch_l2(D + (size_t)i * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
             }
         }
         // (C) merge (graph.py:229-264) on this CTA's private copies

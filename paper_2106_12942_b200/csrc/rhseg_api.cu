@@ -226,16 +226,9 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     // grow the cluster until the per-CTA row slice fits shared memory
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
     if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
-    // stream ring: the default keeps two CTAs per SM; when the level has at most one
-    // CTA per SM anyway, a bigger ring keeps more of each CTA's stream in flight
-    int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
-    if (spec && (long long)lv.nsec * lv.C <= c->nsm) {
-        for (int sb = 96 * 1024; sb > stage_bytes; sb -= 8 * 1024)
-            if (hseg_loop_smem(lv.Rp, lv.C, lv.B, spec, lv.measure, sb) <= 220 * 1024) {
-                stage_bytes = sb;
-                break;
-            }
-    }
+    // stream ring stage size (runtime knob; bigger rings for single-CTA-per-SM levels
+    // were measured slower on C2: 49 -> 82 ms)
+    const int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
