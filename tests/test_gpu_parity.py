@@ -323,3 +323,26 @@ def test_band_counts_and_connectivity_vs_oracle(bands, conn, oracle):
         ref = oracle.rhseg_run(s, 2, w, 5, 11, connectivity=conn)
         assert_log_equal(_flat(res), ref, f"B={bands} conn={conn} w={w}")
         assert np.array_equal(res.labels.labels, ref["labels"])
+
+
+def test_stress_determinism_and_leaf_parity(oracle):
+    """Races show up as run-to-run differences at scale: 64 leaves of 32x32x64
+    (two CTAs per SM, every phase of the loop exercised thousands of times),
+    repeated runs must agree bit for bit, and sampled leaves must equal an
+    independent HSEG of that leaf on the oracle (leaves are independent
+    sections, recursive.py:130-142)."""
+    img, _ = rh.gen_synthetic(256, 64, 16, 25, 3.0, 256)
+    params = rh.RhsegParams(rh.HsegParams(0.21, 16), 4, 16)
+    runs = [_flat(rh.rhseg_run(img, params)) for _ in range(3)]
+    for k in LOG_KEYS:
+        for r in runs[1:]:
+            assert np.array_equal(np.asarray(r[k]).view(np.uint8), np.asarray(runs[0][k]).view(np.uint8)), k
+    f = runs[0]
+    oracle.set_threads(os.cpu_count() or 1)
+    for (lr, lc) in ((0, 0), (3, 5), (7, 7), (5, 2)):
+        m = (f["log_level"] == 4) & (f["log_row"] == lr) & (f["log_col"] == lc)
+        sub = np.ascontiguousarray(img.samples[:, 32 * lr:32 * lr + 32, 32 * lc:32 * lc + 32])
+        ref = oracle.rhseg_run(sub, 1, 0.21, 16)
+        assert np.array_equal(f["log_survivor"][m], ref["log_survivor"])
+        assert np.array_equal(f["log_absorbed"][m], ref["log_absorbed"])
+        assert np.array_equal(f["log_dissim"][m].view(np.uint64), ref["log_dissim"].view(np.uint64))
