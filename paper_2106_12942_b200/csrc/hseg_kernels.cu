@@ -1177,6 +1177,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             }
             if (SPEC && dE) atomicAdd(&sdE, dE);
         }
+        __syncthreads();  // every thread has read cnt[a], cnt[b] (nn) before they change
         if (tid == 0) {
             cnt[a] = (uint32_t)nn;
             cnt[b] = 0u;
