@@ -933,6 +933,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     }
     __syncthreads();
     if (SPEC) E = (long long)(sE0 / 2);
+    // every CTA of the cluster has started (and initialised its shared memory)
+    // before any peer pushes a slot into it with DSMEM stores
+    if (CLUSTER) cluster_barrier();
     if (SPEC && R0 > target) begin_stream();
 
     int a_prev = -1, step = 0, conv = 0;
