@@ -223,6 +223,36 @@ def gen_small_rhseg():
     print("rhseg_small", len(cases), flush=True)
 
 
+def gen_wire_frames():
+    """ASSIGN frames and the unmodified reference worker's RESULT replies
+    (wire.py:103-200, cluster.py:309-327) for a GPU worker speaking the same
+    protocol. Stored as raw bytes; the worker must reproduce RESULT exactly."""
+    from rhseg import wire
+    from rhseg.cluster import WorkerServer
+    from rhseg.sections import SectionId
+
+    cases = []
+    specs = [((16, 8, 4, 6, 3.0, 16), SectionId(3, 1, 2), 0.21, 6),
+             ((32, 12, 4, 6, 3.0, 7), SectionId(2, 0, 1), 0.5, 9),
+             ((12, 3, 2, 3, 1.0, 3), SectionId(1, 0, 0), 0.0, 4)]
+    server = WorkerServer("127.0.0.1", 0)
+    try:
+        for gen, sid, w, tgt in specs:
+            img, _ = gen_synthetic(*gen)
+            payload = wire.AssignPayload(sid, img, w, tgt, "seq", 16).encode()
+            frame = wire.encode_message(wire.ASSIGN, payload)
+            reply = server._run_assign(payload)
+            cases.append((frame, reply))
+    finally:
+        server.stop()
+    arrays = {}
+    for k, (frame, reply) in enumerate(cases):
+        arrays[f"assign_{k}"] = np.frombuffer(frame, np.uint8)
+        arrays[f"result_{k}"] = np.frombuffer(reply, np.uint8)
+    np.savez_compressed(os.path.join(GOLDEN, "wire_frames.npz"), n=len(cases), **arrays)
+    print("wire_frames", [len(r) for _, r in cases])
+
+
 def main(which):
     os.makedirs(GOLDEN, exist_ok=True)
     workers = int(os.environ.get("GOLDEN_WORKERS", "6"))
@@ -238,6 +268,8 @@ def main(which):
         img, _ = gen_synthetic(32, 224, 16, 25, 3.0, 32)
         gen_rhseg("rhseg_32x32x224_L2", img, RhsegParams(HsegParams(0.21, 16), levels=2), fast,
                   "gen_synthetic(32,224,16,25,3.0,32); L=2, w=0.21, target 16 (C3/C4 leaf shape)")
+    if which in ("wire", "all"):
+        gen_wire_frames()
     if which in ("crit2", "all"):
         img, _ = gen_synthetic(64, 16, 4, 6, 3.0, 64)
         gen_rhseg("crit2_64x64x16_L3", img, RhsegParams(HsegParams(0.21, 50), levels=3, section_target_regions=60), fast,
