@@ -38,8 +38,7 @@ def test_tcp_worker_session():
             # a bad assignment is reported, not fatal
             _, payload = worker.decode_message(next(_frames())[0])
             bad = bytearray(payload)
-            bad[5 + 8:5 + 16] = (2.0).hex().encode()[:0] or bytes(8)  # weight 0 keeps it valid; break target instead
-            bad[5 + 16:5 + 20] = (0).to_bytes(4, "little")          # section_target 0 -> ValueError
+            bad[5 + 16:5 + 20] = (0).to_bytes(4, "little")  # section_target 0 -> ValueError
             s.sendall(worker.encode_message(worker.ASSIGN, bytes(bad)))
             t, body = worker.read_message(rd)
             assert t == worker.ERROR and b"ValueError" in body
