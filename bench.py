@@ -238,12 +238,12 @@ def run_ours(args):
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
     if world > 1:
         from paper_2106_12942_b200 import distributed as rdist
 
         return rdist.bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, cpu_sample)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
 
     name = args.workload
     spec, crop, levels, w, t, st = WORKLOADS[name]

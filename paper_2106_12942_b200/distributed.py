@@ -417,25 +417,53 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
 
     from .recursive import HsegParams, RhsegParams
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import ctypes
+    import time
+
+    from bench import MEASURE_OF
+
+    from .synth import gen_synthetic
+
+    # one process per GPU; RHSEG_DIST_BACKEND=gloo lets several ranks share one GPU
+    # (the single-GPU test box) -- collectives then stage through host memory
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    backend = os.environ.get("RHSEG_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     rank, world = dist.get_rank(), dist.get_world_size()
     name = args.workload
     spec, crop, levels, w, t, st = WORKLOADS[name]
     bands, edge, _ = cube_shape(name)
     dev = torch.device("cuda", local)
-    host = torch.empty((bands, edge, edge), dtype=torch.float32, pin_memory=True)
-    make_cube(name, out=host.numpy())
-    cube = host.to(dev)
-    from bench import MEASURE_OF
+    top, blocks = shard_plan(levels, world)
+    blk = blocks[rank]
+    # this rank's image rows only (host memory and H2D scale with 1/world)
+    et = edge >> (top - 1)
+    r0, r1 = (blk[0] * et, (blk[0] + blk[2]) * et) if blk is not None else (0, 0)
+    host = torch.empty((bands, max(r1 - r0, 1), edge), dtype=torch.float32, pin_memory=True)
+    if r1 > r0:
+        if crop is None:
+            gen_synthetic(*spec, out=host.numpy(), rows=(r0, r1))
+        else:
+            host.numpy()[...] = make_cube(name)[:, r0:r1, :]
+    cube = torch.empty((bands, edge, edge), dtype=torch.float32, device=dev)
 
+    def upload():
+        if r1 > r0:
+            cube[:, r0:r1, :].copy_(host[:, :r1 - r0, :], non_blocking=True)
+
+    upload()
     params = RhsegParams(HsegParams(w, t, MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
     sh = ShardedRhseg(params, edge, bands, local)
     flush = torch.empty(2 * 126 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     for _ in range(args.warmup):
         sh.step(cube)
     torch.cuda.synchronize()
-    times = []
+    times, launches = [], 0
+    n = ctypes.c_int64()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
@@ -448,12 +476,33 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
             torch.cuda.synchronize()
             dist.barrier()
             times.append(e0.elapsed_time(e1))
-    ms = torch.tensor([float(np.mean(times))], device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+            sh.runner.lib.rhseg_result_launches(sh.runner.ctx.handle, ctypes.byref(n))
+            launches += int(n.value)
+    # end to end: this rank's rows H2D, the sharded run, logs gathered to rank 0,
+    # root labels D2H on rank 0 (wall clock, max over ranks)
+    lab = np.empty(edge * edge, np.int32)
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        upload()
+        torch.cuda.synchronize()
+        parts = sh.step(cube, gather_logs=True)
+        if rank == 0:
+            from . import _lib
+
+            _lib.check(sh.runner.lib.rhseg_result_labels(sh.runner.ctx.handle, _lib.ptr(lab), None), "labels")
+        torch.cuda.synchronize()
+        e2e.append(time.perf_counter() - t0)
+        del parts
+    vals = torch.tensor([float(np.mean(times)), float(np.median(e2e)) * 1e3, float(launches)], device=dev)
+    mx = vals.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(vals, op=dist.ReduceOp.SUM)
+    ms, e2e_ms, launches_total = float(mx[0]), float(mx[1]), int(vals[2].item())
     if rank == 0:
         npxb = edge * edge * bands
-        top, blocks = shard_plan(levels, world)
         line = {
             "metric": "RHSEG pixel-bands/sec", "value": npxb / (ms * 1e-3), "unit": "pixel-bands/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -462,6 +511,11 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
             "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels,
                        "parallelism": f"subtree sharding: level-{top} subtrees over {world} ranks, NCCL gather to rank 0",
                        "l2": "flushed between timed steps (2x126 MB write)"},
+            "gpu_launches": launches_total,
+            "e2e": {"value": npxb / (e2e_ms * 1e-3), "unit": "pixel-bands/s",
+                    "h2d_bytes_per_step": npxb * 4, "d2h_bytes_per_step": edge * edge * 4,
+                    "ms_per_step": e2e_ms,
+                    "note": "each rank uploads its own rows; merge logs gathered to rank 0 over NCCL"},
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
