@@ -224,11 +224,12 @@ constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
 // arrays with a smaller stream ring, so two CTAs still fit one SM.
 constexpr int kStageBytesTop2 = 20 * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
+constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per merge
 constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
     size_t fref, fxa, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
-        bAj2, bNj2, cx, ring, total;
+        bAj2, bNj2, cx, nbl, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
@@ -261,6 +262,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.bAj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
     L.bNj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
     L.cx = o;    o = align16(o + (top2 ? Rs : 0));
+    L.nbl = o;   o = align16(o + kNbList * 2);  // b's neighbours during a merge
     o = (o + 127) & ~size_t(127);
     L.ring = o;
     o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * stage_bytes + kThreads * 8 : 0;
@@ -526,6 +528,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int* bAj2 = reinterpret_cast<int*>(smem + L.bAj2);
     int* bNj2 = reinterpret_cast<int*>(smem + L.bNj2);
     uint8_t* cx = reinterpret_cast<uint8_t*>(smem + L.cx);
+    unsigned short* nbl = reinterpret_cast<unsigned short*>(smem + L.nbl);
+    int& nnb = misc[13];
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
     double* const mu0 = bt.mu + sec * bt.mu_stride();
@@ -971,6 +975,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     bNj[r] = rpart[1].j == kNoJ ? -1 : rpart[1].j;
                 }
                 ninv = 0;
+                nnb = 0;
                 sScan = 0;
             }
             __syncthreads();
@@ -1029,7 +1034,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 if (bAj[r] >= 0) pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
                 if (SPEC && bNj[r] >= 0) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
             }
-            if (tid == 0) ninv = 0;
+            if (tid == 0) { ninv = 0; nnb = 0; }
             ca = block_min_pair(ca, pscr);
             if (SPEC) cn = block_min_pair(cn, pscr);
         }
@@ -1153,9 +1158,16 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
         uint32_t* ra = adj + (size_t)a * W;
         {
+            // adjacency union (A|B)\{a,b}; b's neighbours are collected first and then
+            // re-pointed b -> a one per thread (not serially per bitset word)
             uint32_t* rbw = adj + (size_t)b * W;
             const int wa = a >> 5, wb = b >> 5;
             const uint32_t ma = 1u << (a & 31), mb = 1u << (b & 31);
+            auto repoint = [&](int n) {
+                uint32_t* rn = adj + (size_t)n * W;
+                if (wa == wb) rn[wa] = (rn[wa] | ma) & ~mb;
+                else { rn[wa] |= ma; rn[wb] &= ~mb; }
+            };
             int dE = 0;
             for (int w = tid; w < W; w += kThreads) {
                 const uint32_t oa = ra[w], ob = rbw[w];
@@ -1168,17 +1180,19 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 }
                 ra[w] = nw;
                 rbw[w] = 0u;
-                uint32_t bits = ob;
+                uint32_t bits = w == wa ? ob & ~ma : ob;
                 while (bits) {
                     const int n = (w << 5) + __ffs(bits) - 1;
                     bits &= bits - 1;
-                    if (n == a) continue;
-                    uint32_t* rn = adj + (size_t)n * W;
-                    if (wa == wb) rn[wa] = (rn[wa] | ma) & ~mb;
-                    else { rn[wa] |= ma; rn[wb] &= ~mb; }
+                    const int k = atomicAdd(&nnb, 1);
+                    if (k < kNbList) nbl[k] = (unsigned short)n;
+                    else repoint(n);  // overflow (very high degree): in place
                 }
             }
             if (SPEC && dE) atomicAdd(&sdE, dE);
+            __syncthreads();
+            const int nb = min(nnb, kNbList);
+            for (int k = tid; k < nb; k += kThreads) repoint(nbl[k]);
         }
         __syncthreads();  // every thread has read cnt[a], cnt[b] (nn) before they change
         if (tid == 0) {
