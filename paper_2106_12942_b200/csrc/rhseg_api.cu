@@ -139,6 +139,10 @@ struct rhseg_ctx {
     // repeated runs of one shape allocate nothing, so no run waits on the driver.
     std::map<int, std::pair<void*, size_t>> bufs;
     size_t dmat_budget = 0;  // bytes the D matrix may use (measured once per ctx)
+    // host-input pipeline (rhseg_run_host): a copy stream and per-chunk streams/events
+    cudaStream_t copy_stream = nullptr;
+    cudaStream_t pstream[8] = {};
+    cudaEvent_t ready[8] = {}, done[9] = {};
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
@@ -326,7 +330,17 @@ static bool profiling() {
     return on;
 }
 
-static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
+// Leaf level fed chunk by chunk from host memory: chunk k (a band of leaf rows)
+// becomes runnable when its upload (event ready[k]) lands; its leaf init, all-pairs
+// D and merge loop then run on stream pstream[k], concurrently with the other
+// chunks and with the remaining uploads.
+struct LeafPipe {
+    int K;
+    const float* d_samples;
+    int edge, cols, row0, col0, conn;
+};
+
+static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* pipe = nullptr) {
     unsigned long long* prof = nullptr;
     if (profiling()) {
         CK(cudaMallocAsync(&prof, 8 * 8, st));
@@ -352,24 +366,55 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st) {
         chunk = std::max<size_t>(1, std::min<size_t>(lv.nsec, c->dmat_bytes / dsec));
     }
     lv.sb.D = static_cast<double*>(c->dmat);
-    for (size_t s0 = 0; s0 < (size_t)lv.nsec; s0 += chunk) {
-        const int n = (int)std::min(chunk, (size_t)lv.nsec - s0);
-        SectionBatch b = lv.sb;
-        b.sec0 = (int)s0;
-        {
-            PhaseTimer t(c, 1, st);
-            launch_dinit(b, n, lv.R0max, st);
-            c->launches += 1;
-        }
-        CK(cudaGetLastError());
-        {
-            PhaseTimer t(c, 2, st);
-            int e = launch_hseg_loop(b, n, st);
-            c->launches += 1;
+    if (pipe && chunk == (size_t)lv.nsec) {
+        const int per = lv.nsec / pipe->K;
+        PhaseTimer t(c, 2, st);
+        CK(cudaEventRecord(c->done[pipe->K], st));  // level buffers are initialised on st
+        for (int k = 0; k < pipe->K; ++k) {
+            cudaStream_t sk = c->pstream[k];
+            CK(cudaStreamWaitEvent(sk, c->done[pipe->K], 0));
+            CK(cudaStreamWaitEvent(sk, c->ready[k], 0));
+            SectionBatch b = lv.sb;
+            b.sec0 = k * per;
+            launch_leaf_init(b, pipe->d_samples, pipe->edge, pipe->cols, pipe->row0, pipe->col0, pipe->conn, sk,
+                             per);
+            b.D = lv.sb.D + (size_t)k * per * (dsec / 8);
+            launch_dinit(b, per, lv.R0max, sk);
+            int e = launch_hseg_loop(b, per, sk);
             if (e != cudaSuccess)
                 return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
+            c->launches += 3;
+            CK(cudaEventRecord(c->done[k], sk));
+            CK(cudaStreamWaitEvent(st, c->done[k], 0));
         }
         CK(cudaGetLastError());
+    } else {
+        if (pipe) {  // D does not fit every section at once: upload everything, then chunk
+            for (int k = 0; k < pipe->K; ++k) CK(cudaStreamWaitEvent(st, c->ready[k], 0));
+            SectionBatch b = lv.sb;
+            launch_leaf_init(b, pipe->d_samples, pipe->edge, pipe->cols, pipe->row0, pipe->col0, pipe->conn, st);
+            c->launches += 1;
+        }
+        for (size_t s0 = 0; s0 < (size_t)lv.nsec; s0 += chunk) {
+            const int n = (int)std::min(chunk, (size_t)lv.nsec - s0);
+            SectionBatch b = lv.sb;
+            b.sec0 = (int)s0;
+            b.D = lv.sb.D;
+            {
+                PhaseTimer t(c, 1, st);
+                launch_dinit(b, n, lv.R0max, st);
+                c->launches += 1;
+            }
+            CK(cudaGetLastError());
+            {
+                PhaseTimer t(c, 2, st);
+                int e = launch_hseg_loop(b, n, st);
+                c->launches += 1;
+                if (e != cudaSuccess)
+                    return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
+            }
+            CK(cudaGetLastError());
+        }
     }
     {
         PhaseTimer t(c, 3, st);
@@ -564,8 +609,22 @@ static int finish_run(rhseg_ctx* c, cudaStream_t st) {
 // section grid; top = 1 with the 1x1 block is SequentialExecutor.execute
 // (recursive.py:173-209). A block of level-`top` subtrees is the unit a rank
 // owns under multi-GPU sharding.
+static int ensure_pipeline(rhseg_ctx* c) {
+    if (c->copy_stream) return RHSEG_OK;
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 8; ++k) {
+        CK(cudaStreamCreateWithFlags(&c->pstream[k], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ready[k], cudaEventDisableTiming));
+    }
+    for (int k = 0; k < 9; ++k) CK(cudaEventCreateWithFlags(&c->done[k], cudaEventDisableTiming));
+    return RHSEG_OK;
+}
+
+// h_samples (optional): the same cube in host memory; the leaf level is then fed
+// chunk by chunk while it uploads into d_samples (rhseg_run_host).
 static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int bands, const rhseg_params* p,
-                           int top, int r0, int c0, int nr, int nc, cudaStream_t st) {
+                           int top, int r0, int c0, int nr, int nc, cudaStream_t st,
+                           const float* h_samples = nullptr) {
     int rc = validate(p, edge, bands);
     if (rc) return rc;
     const int L = p->levels;
@@ -607,18 +666,36 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster, 0);
         RHSEG_TRACE("leaves: alloc done");
         if (rc) return rc;
-        {
-            PhaseTimer t(c, 0, st);
-            launch_leaf_init(lv.sb, d_samples, edge, lv.cols, lv.row0, lv.col0, p->connectivity, st);
-            c->launches += 1;
-        }
-        CK(cudaGetLastError());
-        if (L == 1) {
-            rc = snapshot_root(c, lv, st);
+        const bool piped = h_samples && L >= 2 && top == 1;
+        if (piped) {
+            // upload in K bands of leaf rows on the copy stream; chunk k starts as soon
+            // as its rows land (run_level / LeafPipe)
+            rc = ensure_pipeline(c);
+            if (rc) return rc;
+            LeafPipe pipe{std::min(8, lv.rows), d_samples, edge, lv.cols, lv.row0, lv.col0, p->connectivity};
+            const size_t rows = (size_t)edge / pipe.K, plane = (size_t)edge * edge;
+            for (int k = 0; k < pipe.K; ++k) {
+                const size_t off = (size_t)k * rows * edge;
+                CK(cudaMemcpy2DAsync(const_cast<float*>(d_samples) + off, plane * 4, h_samples + off, plane * 4,
+                                     rows * edge * 4, (size_t)bands, cudaMemcpyHostToDevice, c->copy_stream));
+                CK(cudaEventRecord(c->ready[k], c->copy_stream));
+            }
+            rc = run_level(c, lv, st, &pipe);
+            if (rc) return rc;
+        } else {
+            {
+                PhaseTimer t(c, 0, st);
+                launch_leaf_init(lv.sb, d_samples, edge, lv.cols, lv.row0, lv.col0, p->connectivity, st);
+                c->launches += 1;
+            }
+            CK(cudaGetLastError());
+            if (L == 1) {
+                rc = snapshot_root(c, lv, st);
+                if (rc) return rc;
+            }
+            rc = run_level(c, lv, st);
             if (rc) return rc;
         }
-        rc = run_level(c, lv, st);
-        if (rc) return rc;
     }
     rc = upper_levels(c, p, top, st);
     if (rc) return rc;
@@ -688,6 +765,14 @@ int rhseg_ctx_destroy(rhseg_ctx* c) {
         if (kv.second.first) cudaFree(kv.second.first);
     c->bufs.clear();
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->copy_stream) {
+        cudaStreamDestroy(c->copy_stream);
+        for (int k = 0; k < 8; ++k) {
+            cudaStreamDestroy(c->pstream[k]);
+            cudaEventDestroy(c->ready[k]);
+        }
+        for (int k = 0; k < 9; ++k) cudaEventDestroy(c->done[k]);
+    }
     cudaStreamDestroy(c->stream);
     delete c;
     return RHSEG_OK;
@@ -974,8 +1059,12 @@ int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t b
         if (rc) return rc;
         d = static_cast<float*>(p);
     }
-    CK(cudaMemcpyAsync(d, h_samples, bytes, cudaMemcpyHostToDevice, st));
-    rc = run_device_impl(c, d, edge, bands, p, 1, 0, 0, 1, 1, st);
+    if (p->levels >= 2) {  // leaf chunks start while the rest of the cube uploads
+        rc = run_device_impl(c, d, edge, bands, p, 1, 0, 0, 1, 1, st, h_samples);
+    } else {
+        CK(cudaMemcpyAsync(d, h_samples, bytes, cudaMemcpyHostToDevice, st));
+        rc = run_device_impl(c, d, edge, bands, p, 1, 0, 0, 1, 1, st);
+    }
     if (rc) return rc;
     rc = copy_log(c, log_survivor, log_absorbed, log_dissim, log_kind, st);
     if (rc) return rc;

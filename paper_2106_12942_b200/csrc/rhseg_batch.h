@@ -70,8 +70,9 @@ size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_by
 int hseg_loop_stage_bytes(bool spec, int C, int measure);  // default ring stage size
 int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
 bool hseg_use_f32(bool spec, int C, int measure);  // the loop streams fp32 filter means
+// sections [b.sec0, b.sec0 + count) of the leaf level (count < 0: through the end)
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
-                      int col0, int connectivity, cudaStream_t st);
+                      int col0, int connectivity, cudaStream_t st, int count = -1);
 void launch_resolve(const SectionBatch& b, cudaStream_t st);
 // Parent grid rows x pcols, child grid (2 rows) x (2 pcols), both row-major.
 void launch_stitch(const SectionBatch& child, int child_cols, const SectionBatch& parent,

@@ -21,7 +21,7 @@ namespace rhseg {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
 leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int cols, int row0, int col0, int conn) {
-    const int sec = blockIdx.x;
+    const int sec = bt.sec0 + blockIdx.x;  // sections [sec0, sec0 + gridDim.x) of the level
     const int e = bt.edge, R0 = e * e, B = bt.B, Rp = bt.Rp, W = bt.W;
     const int orow = (row0 + sec / cols) * e, ocol = (col0 + sec % cols) * e;
     uint32_t* cnt = bt.count + (size_t)sec * Rp;
@@ -83,9 +83,10 @@ leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int col
 }
 
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0, int col0,
-                      int connectivity, cudaStream_t st) {
-    if (b.nsec == 0) return;
-    leaf_init_kernel<<<b.nsec, kThreads, 0, st>>>(b, cube, img_edge, cols, row0, col0, connectivity);
+                      int connectivity, cudaStream_t st, int count) {
+    const int n = count < 0 ? b.nsec - b.sec0 : count;
+    if (n <= 0) return;
+    leaf_init_kernel<<<n, kThreads, 0, st>>>(b, cube, img_edge, cols, row0, col0, connectivity);
 }
 
 // ---------------------------------------------------------------------------
