@@ -187,10 +187,6 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // cost more than the halved stream saves. profiles/r01_loop_variants.md.
 #define RHSEG_F32FILTER 0
 #endif
-#if defined(RHSEG_DIRECT) && RHSEG_DIRECT
-#undef RHSEG_F32FILTER
-#define RHSEG_F32FILTER 0  // the unstaged experiment streams fp64 only
-#endif
 #ifndef RHSEG_COMPACT_K
 #define RHSEG_COMPACT_K 16  // compaction threshold: holes^2 >= K * S (K=16: C4 loop 874 -> 864 ms)
 #endif
@@ -203,21 +199,6 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #ifndef RHSEG_STAGE_KB
 #define RHSEG_STAGE_KB 32
 #endif
-#ifndef RHSEG_PREFETCH_KB
-#define RHSEG_PREFETCH_KB 0
-#endif
-#ifndef RHSEG_EMPTY_BARRIERS
-#define RHSEG_EMPTY_BARRIERS 0
-#endif
-#ifndef RHSEG_DIRECT
-#define RHSEG_DIRECT 0
-#endif
-#ifndef RHSEG_UNROLL
-#define RHSEG_UNROLL 8
-#endif
-#ifndef RHSEG_EARLY_STREAM
-#define RHSEG_EARLY_STREAM 1
-#endif
 constexpr int kStages = RHSEG_STAGES;
 constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
 // SAM keeps the two best partners per row (TOP2 below) and pays for those
@@ -225,7 +206,6 @@ constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
 constexpr int kStageBytesTop2 = 20 * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per merge
-constexpr int kPrefetchBytes = RHSEG_PREFETCH_KB * 1024;  // L2 prefetch distance of the stream per CTA
 
 struct LoopSmem {
     size_t fref, fxa, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
@@ -245,7 +225,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.spart = o; o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
-    L.bars = o;  o += 2 * kStages * 8;  // full[kStages], empty[kStages]
+    L.bars = o;  o += kStages * 8;  // full[kStages]
     L.mua = o;   o = align16(o + (size_t)B * 8);
     L.bAd = o;   o = align16(o + Rs * 8);
     L.bNd = o;   o = align16(o + Rs * 8);
@@ -265,7 +245,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.nbl = o;   o = align16(o + kNbList * 2);  // b's neighbours during a merge
     o = (o + 127) & ~size_t(127);
     L.ring = o;
-    o += (spec && !RHSEG_DIRECT) ? (size_t)kStages * stage_bytes + kThreads * 8 : 0;
+    o += spec ? (size_t)kStages * stage_bytes + kThreads * 8 : 0;
     L.total = o;
     return L;
 }
@@ -471,7 +451,6 @@ struct StreamState {
     int holes;
     int cur;          // which mean buffer (mu / mu2) holds the compacted columns
     int S2, KB, nst;  // current step's geometry
-    int pf, PF;       // next band row to prefetch into L2 / prefetch distance in rows
     uint32_t base;    // first stage of the current step
 };
 
@@ -510,7 +489,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int& sScan = misc[4];
     RowBest* rpart = reinterpret_cast<RowBest*>(smem + L.rpart);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);  // full: bulk bytes landed
-    uint64_t* ebars = bars + kStages;                                 // empty: all warps read the slot
     double* mua = reinterpret_cast<double*>(smem + L.mua);
     double* bAd = reinterpret_cast<double*>(smem + L.bAd);
     double* bNd = reinterpret_cast<double*>(smem + L.bNd);
@@ -789,15 +767,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // ---- streaming ring (SPEC) ----
     // Stage `i` of the current step into ring slot abs_stage % kStages. Called by
     // all lanes of warp 0: lane 0 arms the full barrier, the lanes issue one bulk
-    // copy per band row in parallel, and rows kPrefetch bytes further ahead are
-    // prefetched into L2 so the next stages' copies hit L2 instead of HBM.
+    // copy per band row in parallel.
     auto issue_stage = [&](uint32_t abs_stage, int i) {
         const int sl = (int)(abs_stage % kStages);
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
         const uint32_t rowb = (uint32_t)ss.S2 * (uint32_t)ES;
-        if (RHSEG_EMPTY_BARRIERS && abs_stage >= (uint32_t)kStages)
-            mbar_wait(&ebars[sl], ((abs_stage - kStages) / kStages) & 1u);
         if (lane == 0) {
             fence_proxy_async_shared();
             mbar_arrive_expect_tx(&bars[sl], rowb * (uint32_t)kb);
@@ -807,11 +782,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         const SE* src = (ss.cur ? sb1 : sb0) + lo;
         for (int kk = lane; kk < kb; kk += 32)
             bulk_g2s(dst + (size_t)kk * rowb, src + (size_t)(k0 + kk) * Rp, rowb, &bars[sl]);
-        if (kPrefetchBytes > 0) {
-            const int p0 = max(k0 + kb, ss.pf), p1 = min(B, k0 + kb + ss.PF);
-            for (int k = p0 + lane; k < p1; k += 32) bulk_prefetch_l2(src + (size_t)k * Rp, rowb);
-            ss.pf = max(ss.pf, p1);
-        }
     };
     // Block-wide exclusive scan of 0/1 flags (two __syncthreads).
     auto block_scan = [&](int v, int& total) {
@@ -871,9 +841,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * ES))) : B;
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
-        ss.pf = 0;
-        ss.PF = (ss.S2 > 0 && kPrefetchBytes > 0) ? min(B, max(1, kPrefetchBytes / (ss.S2 * ES))) : 0;
-        const int pre = RHSEG_DIRECT ? 0 : min(kStages, ss.nst);
+        const int pre = min(kStages, ss.nst);
         if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
         ss.issued += pre;
@@ -890,7 +858,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (tid == 0)
             for (int s = 0; s < kStages; ++s) {
                 mbar_init(&bars[s], 1);
-                mbar_init(&ebars[s], kWarps);
             }
         mbar_init_fence();
     }
@@ -1099,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (a < 0) {
             conv = 1;
             if (SPEC) {  // drain the copies put in flight for this step
-                for (int i = 0; i < (RHSEG_DIRECT ? 0 : min(kStages, ss.nst)); ++i) {
+                for (int i = 0; i < min(kStages, ss.nst); ++i) {
                     const uint32_t g = ss.base + i;
                     mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
                 }
@@ -1332,37 +1299,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 isadj[q] = valid[q] && ((ra[j >> 5] >> (j & 31)) & 1u);
                 s[q] = 0.0;
             }
-#if RHSEG_DIRECT
-            {
-                // direct coalesced loads of the compacted columns, RHSEG_UNROLL bands in
-                // flight per thread (no shared-memory staging, no block barriers)
-                const double* base = (ss.cur ? mu1 : mu0) + lo + tid;
-                switch (nq) {
-#define RHSEG_DIRECT_NQ(NQC, U)                                                              \
-    case NQC: {                                                                              \
-        bool ok[NQC];                                                                        \
-        _Pragma("unroll") for (int q = 0; q < NQC; ++q) ok[q] = tid + q * kThreads < ss.S;   \
-        for (int k0 = 0; k0 < B; k0 += U) {                                                  \
-            double v[U][NQC];                                                                \
-            _Pragma("unroll") for (int u = 0; u < U; ++u)                                    \
-                _Pragma("unroll") for (int q = 0; q < NQC; ++q)                              \
-                    v[u][q] = (ok[q] && k0 + u < B) ? __ldcs(base + (size_t)(k0 + u) * Rp + q * kThreads) : 0.0; \
-            _Pragma("unroll") for (int u = 0; u < U; ++u) {                                  \
-                if (k0 + u < B) {                                                            \
-                    const double m = mua[k0 + u];                                            \
-                    _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, v[u][q]); \
-                }                                                                            \
-            }                                                                                \
-        }                                                                                    \
-    } break;
-                    RHSEG_DIRECT_NQ(1, RHSEG_UNROLL) RHSEG_DIRECT_NQ(2, RHSEG_UNROLL)
-                    RHSEG_DIRECT_NQ(3, RHSEG_UNROLL) RHSEG_DIRECT_NQ(4, RHSEG_UNROLL)
-                    RHSEG_DIRECT_NQ(5, 4) RHSEG_DIRECT_NQ(6, 4) RHSEG_DIRECT_NQ(7, 4) RHSEG_DIRECT_NQ(8, 4)
-#undef RHSEG_DIRECT_NQ
-                    default: break;
-                }
-            }
-#else
             for (int i = 0; i < ss.nst; ++i) {
                 const uint32_t g = ss.base + i;
                 mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
@@ -1384,18 +1320,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #undef RHSEG_CONSUME
                     default: break;
                 }
-#if RHSEG_EMPTY_BARRIERS
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&ebars[g % kStages]);  // this warp is done with the slot
-#else
                 __syncthreads();  // slot g % kStages is free again
-#endif
                 if (i + kStages < ss.nst) {
                     if (warp == 0) issue_stage(g + kStages, i + kStages);
                 }
             }
             ss.issued += max(0, ss.nst - kStages);
-#endif
             if (F32) {
                 // an interval around every d(a, j) goes to D; offers compare
                 // intervals and only an overlap with row j's cached best is resolved
@@ -1547,12 +1477,11 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (SPEC && b >= lo && b < hi) ss.holes += 1;
         __syncthreads();
         // next step's stream overlaps the rescans below and the next argmin
-        if (RHSEG_EARLY_STREAM && SPEC && R0 - (step + 1) > target) begin_stream();
+        if (SPEC && R0 - (step + 1) > target) begin_stream();
 
         mark(3);
         a_prev = a;
         ++step;
-        if (!RHSEG_EARLY_STREAM && SPEC && R0 - step > target) begin_stream();
     }
     if (CLUSTER) cluster_barrier();  // keep our slots alive until every peer is done reading
     if (bt.prof && tid == 0) {
