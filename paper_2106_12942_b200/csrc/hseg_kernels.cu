@@ -59,10 +59,12 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
 
     // band staging (sA, sB) and the transpose tile (sT) share one buffer: sT is
     // only touched after the last band chunk's trailing __syncthreads().
-    __shared__ double smraw[kTile * (kTile + 1)];
+    __shared__ __align__(16) double smraw[kTile * (kTile + 1)];
     double (*sA)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw);
     double (*sB)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw + kKB * kTile);
     double (*sT)[kTile + 1] = reinterpret_cast<double (*)[kTile + 1]>(smraw);
+    // thread (tx, ty) owns rows i0 + 4 ty + p and columns j0 + 4 tx + q: both operand
+    // quads are contiguous in shared memory (two 16-byte loads each)
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     double acc[4][4];
 #pragma unroll
@@ -79,13 +81,16 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
             sB[kk][r] = in ? mu[(size_t)(k0 + kk) * Rp + j0 + r] : 0.0;
         }
         __syncthreads();
-        for (int kk = 0; kk < kn; ++kk) {
-            double a[4], b[4];
+        // always kKB bands: the zero padding of a short last chunk adds exactly +0.0
+        // to every accumulator (never -0.0), an identity, so the bits are unchanged
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a[q] = sA[kk][ty + 16 * q];
-                b[q] = sB[kk][tx + 16 * q];
-            }
+        for (int kk = 0; kk < kKB; ++kk) {
+            const double2 a01 = *reinterpret_cast<const double2*>(&sA[kk][4 * ty]);
+            const double2 a23 = *reinterpret_cast<const double2*>(&sA[kk][4 * ty + 2]);
+            const double2 b01 = *reinterpret_cast<const double2*>(&sB[kk][4 * tx]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&sB[kk][4 * tx + 2]);
+            const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -95,17 +100,17 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-        const int i = i0 + ty + 16 * p;
+        const int i = i0 + 4 * ty + p;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int j = j0 + tx + 16 * q;
+            const int j = j0 + 4 * tx + q;
             double d = 0.0;
             if (i < R0 && j < R0) {
                 d = pair_finish<M>((double)cnt[i], (double)cnt[j], acc[p][q], M == kSam ? n2[i] : 0.0,
                                    M == kSam ? n2[j] : 0.0);
                 D[(size_t)i * Rp + j] = d;
             }
-            sT[ty + 16 * p][tx + 16 * q] = d;
+            sT[4 * ty + p][4 * tx + q] = d;
         }
     }
     if (ti == tj) return;  // diagonal tile already holds both orders (d is bitwise symmetric)
