@@ -179,7 +179,7 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 
 // Streaming ring for the spectral row-a pass (w > 0): the live regions' mean
 // columns of one CTA are streamed band-chunk by band-chunk from HBM with bulk
-// async copies (TMA 1D) into kStages x kStageBytes of shared memory.
+// async copies (TMA 1D) into a ring of nstages x stage_bytes of shared memory.
 // Measured on C4 (tools/ab_variants.py, profiles/r01_loop_variants.md): 2 x 32 KB
 // stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
@@ -204,7 +204,7 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #ifndef RHSEG_STAGE_KB
 #define RHSEG_STAGE_KB 32
 #endif
-constexpr int kStages = RHSEG_STAGES;
+constexpr int kMaxStages = 4;  // ring depth for levels with at most one CTA per SM
 constexpr int kStageBytes = RHSEG_STAGE_KB * 1024;
 // SAM keeps the two best partners per row (TOP2 below) and pays for those
 // arrays with a smaller stream ring, so two CTAs still fit one SM.
@@ -219,7 +219,7 @@ struct LoopSmem {
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
 __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2, bool f32,
-                                                     int stage_bytes) {
+                                                     int stage_bytes, int nstages) {
     const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
     size_t o = 0;
@@ -230,7 +230,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.spart = o; o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
-    L.bars = o;  o += kStages * 8;  // full[kStages]
+    L.bars = o;  o += kMaxStages * 8;  // full[nstages]
     L.mua = o;   o = align16(o + (size_t)B * 8);
     L.bAd = o;   o = align16(o + Rs * 8);
     L.bNd = o;   o = align16(o + Rs * 8);
@@ -250,7 +250,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.nbl = o;   o = align16(o + kNbList * 2);  // b's neighbours during a merge
     o = (o + 127) & ~size_t(127);
     L.ring = o;
-    o += spec ? (size_t)kStages * stage_bytes + kThreads * 8 : 0;
+    o += spec ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;
     L.total = o;
     return L;
 }
@@ -261,10 +261,13 @@ __host__ __device__ inline bool use_f32(bool spec, int C, int measure) {
 int hseg_loop_stage_bytes(bool spec, int C, int measure) {
     return use_top2(spec, C, measure) ? kStageBytesTop2 : kStageBytes;
 }
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes) {
-    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure), stage_bytes)
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes, int nstages) {
+    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure), stage_bytes,
+                            nstages)
         .total;
 }
+int hseg_loop_max_stages() { return kMaxStages; }
+int hseg_loop_default_stages() { return RHSEG_STAGES; }
 bool hseg_use_f32(bool spec, int C, int measure) { return use_f32(spec, C, measure); }
 int hseg_loop_max_rows() { return kMaxSlots; }
 
@@ -480,8 +483,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     constexpr bool F32 = RHSEG_F32FILTER && SPEC && !CLUSTER && M != kSam;
     using SE = typename std::conditional<F32, float, double>::type;  // streamed element
     constexpr int ES = (int)sizeof(SE);
-    const int SB = bt.stage_bytes;  // ring stage size chosen by the host (occupancy-aware)
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32, SB);
+    const int SB = bt.stage_bytes;  // ring stage size and depth chosen by the host
+    const int NS = bt.nstages;      // (deeper ring when the level has <= 1 CTA per SM)
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32, SB, NS);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -770,11 +774,11 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     };
 
     // ---- streaming ring (SPEC) ----
-    // Stage `i` of the current step into ring slot abs_stage % kStages. Called by
+    // Stage `i` of the current step into ring slot abs_stage % NS. Called by
     // all lanes of warp 0: lane 0 arms the full barrier, the lanes issue one bulk
     // copy per band row in parallel.
     auto issue_stage = [&](uint32_t abs_stage, int i) {
-        const int sl = (int)(abs_stage % kStages);
+        const int sl = (int)(abs_stage % NS);
         const int k0 = i * ss.KB;
         const int kb = min(ss.KB, B - k0);
         const uint32_t rowb = (uint32_t)ss.S2 * (uint32_t)ES;
@@ -835,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         ss.cur ^= 1;
     };
 
-    // Geometry of the next step's stream + its first kStages band chunks in flight
+    // Geometry of the next step's stream + its first NS band chunks in flight
     // (compacting first when >= 25% of the own columns are holes).
     auto begin_stream = [&]() {
         // compact when holes >= 2 sqrt(S): balances the streamed holes (~1/sqrt(S) of
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         ss.KB = ss.S2 > 0 ? max(1, min(B, SB / (ss.S2 * ES))) : B;
         ss.nst = ss.S2 > 0 ? (B + ss.KB - 1) / ss.KB : 0;
         ss.base = ss.issued;
-        const int pre = min(kStages, ss.nst);
+        const int pre = min(NS, ss.nst);
         if (warp == 0)
             for (int i = 0; i < pre; ++i) issue_stage(ss.base + i, i);
         ss.issued += pre;
@@ -861,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
         ss.S = max(0, hi - lo);
         if (tid == 0)
-            for (int s = 0; s < kStages; ++s) {
+            for (int s = 0; s < NS; ++s) {
                 mbar_init(&bars[s], 1);
             }
         mbar_init_fence();
@@ -1071,9 +1075,9 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (a < 0) {
             conv = 1;
             if (SPEC) {  // drain the copies put in flight for this step
-                for (int i = 0; i < min(kStages, ss.nst); ++i) {
+                for (int i = 0; i < min(NS, ss.nst); ++i) {
                     const uint32_t g = ss.base + i;
-                    mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
+                    mbar_wait(&bars[g % NS], (g / NS) & 1u);
                 }
             }
             break;
@@ -1306,8 +1310,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             }
             for (int i = 0; i < ss.nst; ++i) {
                 const uint32_t g = ss.base + i;
-                mbar_wait(&bars[g % kStages], (g / kStages) & 1u);
-                const SE* tile = reinterpret_cast<const SE*>(ring) + (size_t)(g % kStages) * (SB / ES);
+                mbar_wait(&bars[g % NS], (g / NS) & 1u);
+                const SE* tile = reinterpret_cast<const SE*>(ring) + (size_t)(g % NS) * (SB / ES);
                 const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
                 // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
                 // accumulate garbage that the epilogue discards via valid[])
@@ -1325,12 +1329,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 #undef RHSEG_CONSUME
                     default: break;
                 }
-                __syncthreads();  // slot g % kStages is free again
-                if (i + kStages < ss.nst) {
-                    if (warp == 0) issue_stage(g + kStages, i + kStages);
+                __syncthreads();  // slot g % NS is free again
+                if (i + NS < ss.nst) {
+                    if (warp == 0) issue_stage(g + NS, i + NS);
                 }
             }
-            ss.issued += max(0, ss.nst - kStages);
+            ss.issued += max(0, ss.nst - NS);
             if (F32) {
                 // an interval around every d(a, j) goes to D; offers compare
                 // intervals and only an overlap with row j's cached best is resolved
@@ -1505,7 +1509,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
 
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
-    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure, b.stage_bytes);
+    const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure, b.stage_bytes, b.nstages);
     void (*kern)(SectionBatch);
 #define RHSEG_PICK(M)                                                                              \
     if (b.C > 1) kern = b.spec ? hseg_loop_kernel<true, true, M> : hseg_loop_kernel<true, false, M>; \

@@ -223,16 +223,22 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
     const bool spec = weight > 0.0;
     auto fits = [&](int C) {
-        return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure, hseg_loop_stage_bytes(spec, C, lv.measure)) <=
+        return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure, hseg_loop_stage_bytes(spec, C, lv.measure),
+                              hseg_loop_default_stages()) <=
                    220 * 1024 &&
                (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
     };
     // grow the cluster until the per-CTA row slice fits shared memory
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
     if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
-    // stream ring stage size (runtime knob; bigger rings for single-CTA-per-SM levels
-    // were measured slower on C2: 49 -> 82 ms)
+    // stream ring: two stages keep two CTAs per SM; a level with at most one CTA
+    // per SM anyway gets a deeper ring (more of each CTA's stream in flight).
+    // (Bigger stages instead were measured slower on C2: 49 -> 82 ms.)
     const int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
+    int nstages = hseg_loop_default_stages();
+    if (spec && (long long)lv.nsec * lv.C <= c->nsm &&
+        hseg_loop_smem(lv.Rp, lv.C, lv.B, spec, lv.measure, stage_bytes, hseg_loop_max_stages()) <= 220 * 1024)
+        nstages = hseg_loop_max_stages();
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
@@ -279,6 +285,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.npx = (int)npx;
     b.spec = spec ? 1 : 0;
     b.stage_bytes = stage_bytes;
+    b.nstages = nstages;
     b.measure = lv.measure;
     b.nrm2 = lv.measure == 2 ? reinterpret_cast<double*>(K + oN2) : nullptr;
     b.weight = weight;

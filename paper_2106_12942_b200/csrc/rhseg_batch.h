@@ -32,6 +32,7 @@ struct SectionBatch {
     int spec;      // spectral stage on (weight > 0)
     int measure;   // 0 sqrt-bsmse (reference), 1 euclidean, 2 sam (extensions)
     int stage_bytes;  // merge-loop stream ring stage size (host-chosen)
+    int nstages;      // merge-loop stream ring depth (host-chosen)
     double weight; // spectral_weight (engine.py:33)
     const int* R0;       // [nsec] initial live regions
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
@@ -66,7 +67,9 @@ struct SectionBatch {
 // Kernel launchers (hseg_kernels.cu / section_kernels.cu). All stream-ordered.
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
-size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes);
+size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes, int nstages);
+int hseg_loop_max_stages();
+int hseg_loop_default_stages();
 int hseg_loop_stage_bytes(bool spec, int C, int measure);  // default ring stage size
 int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
 bool hseg_use_f32(bool spec, int C, int measure);  // the loop streams fp32 filter means
