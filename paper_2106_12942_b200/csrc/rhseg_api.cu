@@ -231,14 +231,12 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     // grow the cluster until the per-CTA row slice fits shared memory
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
     if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
-    // stream ring: two stages keep two CTAs per SM; a level with at most one CTA
-    // per SM anyway gets a deeper ring (more of each CTA's stream in flight).
-    // (Bigger stages instead were measured slower on C2: 49 -> 82 ms.)
+    // stream ring geometry (runtime knobs). Deeper (4 x 32 KB) or bigger (2 x 96 KB)
+    // rings for levels with at most one CTA per SM were both measured slower on C2
+    // (47 -> 87 / 82 ms): the shared-memory carveout takes the L1 that the
+    // adjacency and sums accesses live in.
     const int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
-    int nstages = hseg_loop_default_stages();
-    if (spec && (long long)lv.nsec * lv.C <= c->nsm &&
-        hseg_loop_smem(lv.Rp, lv.C, lv.B, spec, lv.measure, stage_bytes, hseg_loop_max_stages()) <= 220 * 1024)
-        nstages = hseg_loop_max_stages();
+    const int nstages = hseg_loop_default_stages();
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
