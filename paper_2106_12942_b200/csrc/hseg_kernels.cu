@@ -214,7 +214,7 @@ constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per me
 
 struct LoopSmem {
     size_t fref, fxa, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
-        bAj2, bNj2, cx, nbl, ring, total;
+        bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
@@ -248,6 +248,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.bNj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
     L.cx = o;    o = align16(o + (top2 ? Rs : 0));
     L.nbl = o;   o = align16(o + kNbList * 2);  // b's neighbours during a merge
+    L.sra = o;   o = align16(o + (size_t)(Rp / 32) * 4);  // a's new adjacency row (row-a pass)
     o = (o + 127) & ~size_t(127);
     L.ring = o;
     o += spec ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;
@@ -516,6 +517,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int* bNj2 = reinterpret_cast<int*>(smem + L.bNj2);
     uint8_t* cx = reinterpret_cast<uint8_t*>(smem + L.cx);
     unsigned short* nbl = reinterpret_cast<unsigned short*>(smem + L.nbl);
+    uint32_t* sra = reinterpret_cast<uint32_t*>(smem + L.sra);
     int& nnb = misc[13];
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
@@ -1155,6 +1157,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     if (w == wb && (oa & mb)) dE += 1;
                 }
                 ra[w] = nw;
+                sra[w] = nw;
                 rbw[w] = 0u;
                 uint32_t bits = w == wa ? ob & ~ma : ob;
                 while (bits) {
@@ -1305,7 +1308,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 const int j = (q < nq && sl < ss.S) ? col[sl] : -1;
                 jq[q] = j;
                 valid[q] = j >= 0 && j != a && j != b && cnt[j] != 0u;
-                isadj[q] = valid[q] && ((ra[j >> 5] >> (j & 31)) & 1u);
+                isadj[q] = valid[q] && ((sra[j >> 5] >> (j & 31)) & 1u);
                 s[q] = 0.0;
             }
             for (int i = 0; i < ss.nst; ++i) {
