@@ -346,3 +346,40 @@ def test_stress_determinism_and_leaf_parity(oracle):
         assert np.array_equal(f["log_survivor"][m], ref["log_survivor"])
         assert np.array_equal(f["log_absorbed"][m], ref["log_absorbed"])
         assert np.array_equal(f["log_dissim"][m].view(np.uint64), ref["log_dissim"].view(np.uint64))
+
+
+def test_device_resident_path_equals_host_path():
+    """rhseg_run_device (cube already in HBM, the bench's `value` leg) and the
+    pipelined rhseg_run_host (chunked upload, the e2e leg / executor) agree bit
+    for bit (leaf chunks of the host path run on their own streams)."""
+    import torch
+
+    from paper_2106_12942_b200.recursive import collect_result, result_info
+
+    img, _ = rh.gen_synthetic(128, 16, 4, 6, 3.0, 12)
+    params = rh.RhsegParams(rh.HsegParams(0.21, 8), 4, 12)
+    host = _flat(rh.rhseg_run(img, params))
+    ex = rh.B200Executor()
+    cube = torch.from_numpy(np.ascontiguousarray(img.samples)).cuda()
+    ctx = ex.execute_device(cube.data_ptr(), 128, 16, params)
+    torch.cuda.synchronize()
+    dev = _flat(collect_result(ctx, result_info(ctx), 128, 16, 4))
+    for k in LOG_KEYS:
+        assert np.array_equal(np.asarray(host[k]).view(np.uint8), np.asarray(dev[k]).view(np.uint8)), k
+
+
+def test_hseg_step_sequence_equals_hseg_run():
+    """hseg_step through the B3 per-row table kernels (engine.py:309-342) merge by
+    merge reproduces the device loop's hseg_run (engine.py:345-371)."""
+    img, _ = rh.gen_synthetic(12, 5, 4, 6, 3.0, 4)
+    g1 = rh.init_region_graph(img, 8)
+    h = rh.hseg_run(g1, rh.HsegParams(0.21, 20))
+    g2 = rh.init_region_graph(img, 8)
+    steps = []
+    while g2.live_count > 20:
+        rec = rh.hseg_step(g2, rh.HsegParams(0.21, 20))
+        if rec is None:
+            break
+        steps.append((rec.survivor_id, rec.absorbed_id, rec.dissimilarity, int(rec.kind)))
+    assert steps == [(r.survivor_id, r.absorbed_id, r.dissimilarity, int(r.kind)) for r in h.records]
+    assert np.array_equal(g1.pixel_assignment, g2.pixel_assignment)
