@@ -4,7 +4,6 @@ its own process (device time of full RHSEG runs, CUDA events on one stream).
 
     python tools/ab_variants.py c4 A B C ...
 """
-import json
 import os
 import subprocess
 import sys

@@ -1,4 +1,5 @@
-import sys, numpy as np, torch, ctypes
+import sys
+import torch
 sys.path.insert(0, '/root/repo')
 import paper_2106_12942_b200 as rh
 from bench import make_cube
