@@ -1,6 +1,6 @@
 import sys
 import torch
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 import paper_2106_12942_b200 as rh
 from bench import make_cube
 host = torch.empty((224, 2048, 2048), dtype=torch.float32, pin_memory=True)
