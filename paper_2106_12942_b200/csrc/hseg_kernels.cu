@@ -225,8 +225,8 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     size_t o = 0;
     L.slot = o;  o += 2 * sizeof(Slot);
     L.rslot = o; o += 2 * kMaxCluster * sizeof(Slot);  // [step parity][source CTA]
-    L.pscr = o;  o += kWarps * sizeof(Pair);
-    L.rscr = o;  o += kWarps * sizeof(RowBest);
+    L.pscr = o;  o += 2 * kWarps * sizeof(Pair);
+    L.rscr = o;  o += 2 * kWarps * sizeof(RowBest);
     L.spart = o; o += kWarps * sizeof(RowBest);
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
@@ -965,8 +965,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 if (bAj[r] >= 0) { d_unpack(bAd[r], l2, h2); uA = fmin(uA, h2); }
                 if (bNj[r] >= 0) { d_unpack(bNd[r], l2, h2); uN = fmin(uN, h2); }
             }
-            uA = block_min_rb(RowBest{uA, 0}, rscr).d;
-            uN = block_min_rb(RowBest{uN, 0}, rscr).d;
+            {
+                RowBest x{uA, 0}, y{uN, 0};
+                block_min_rb2(x, y, rscr);
+                uA = x.d;
+                uN = y.d;
+            }
             unsigned short* clist = reinterpret_cast<unsigned short*>(inv);
             for (int i = lo + tid; i < hi; i += kThreads) {
                 if (cnt[i] == 0u) continue;
@@ -1003,8 +1007,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 if (e >> 14) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
                 else pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
             }
-            ca = block_min_pair(ca, pscr);
-            cn = block_min_pair(cn, pscr);
+            block_min_pair2(ca, cn, pscr);
         } else {
             for (int i = lo + tid; i < hi; i += kThreads) {
                 if (cnt[i] == 0u || i == a_prev) continue;
@@ -1013,8 +1016,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 if (SPEC && bNj[r] >= 0) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
             }
             if (tid == 0) { ninv = 0; nnb = 0; }
-            ca = block_min_pair(ca, pscr);
-            if (SPEC) cn = block_min_pair(cn, pscr);
+            if (SPEC) block_min_pair2(ca, cn, pscr);
+            else ca = block_min_pair(ca, pscr);
         }
         if (tid == 0) {
             slot[par].selA = ca;
@@ -1359,8 +1362,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 }
                 int* cntF = misc + 10;  // [0] overlaps, [1] a-candidates adjacent, [2] non-adjacent
                 if (tid == 0) { cntF[0] = 0; cntF[1] = 0; cntF[2] = 0; }
-                uA = block_min_rb(RowBest{uA, 0}, rscr).d;
-                uN = block_min_rb(RowBest{uN, 0}, rscr).d;
+                {
+                    RowBest x{uA, 0}, y{uN, 0};
+                    block_min_rb2(x, y, rscr);
+                    uA = x.d;
+                    uN = y.d;
+                }
                 unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);  // overlaps
                 unsigned short* l2 = l1 + Rs;                                 // a's candidates
                 // (l1 and l2 each hold at most one entry per own column)
@@ -1475,8 +1482,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                                        nullptr, pA, pN, inv, &ninv);
             }
         }
-        pA = block_min_rb(pA, rscr);
-        if (SPEC) pN = block_min_rb(pN, rscr);
+        if (SPEC) block_min_rb2(pA, pN, rscr);
+        else pA = block_min_rb(pA, rscr);
         if (tid == 0) {
             rpart[0] = pA;
             rpart[1] = pN;

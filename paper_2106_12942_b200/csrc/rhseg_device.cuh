@@ -205,6 +205,47 @@ __device__ __forceinline__ Pair block_min_pair(Pair v, Pair* scratch) {
     return r;
 }
 
+// Two block-wide minima with one shared exchange (scratch: 2 * kWarps entries).
+__device__ __forceinline__ void block_min_pair2(Pair& a, Pair& b, Pair* scratch) {
+    a = warp_min_pair(a);
+    b = warp_min_pair(b);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        scratch[warp] = a;
+        scratch[kWarps + warp] = b;
+    }
+    __syncthreads();
+    Pair ra = scratch[0], rb = scratch[kWarps];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) {
+        if (pair_less(scratch[w], ra)) ra = scratch[w];
+        if (pair_less(scratch[kWarps + w], rb)) rb = scratch[kWarps + w];
+    }
+    __syncthreads();
+    a = ra;
+    b = rb;
+}
+__device__ __forceinline__ void block_min_rb2(RowBest& a, RowBest& b, RowBest* scratch) {
+    a = warp_min_rb(a);
+    b = warp_min_rb(b);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        scratch[warp] = a;
+        scratch[kWarps + warp] = b;
+    }
+    __syncthreads();
+    RowBest ra = scratch[0], rb = scratch[kWarps];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) {
+        const RowBest c = scratch[w], d = scratch[kWarps + w];
+        if (c.d < ra.d || (c.d == ra.d && c.j < ra.j)) ra = c;
+        if (d.d < rb.d || (d.d == rb.d && d.j < rb.j)) rb = d;
+    }
+    __syncthreads();
+    a = ra;
+    b = rb;
+}
+
 // ---------------------------------------------------------------------------
 // Thread-block-cluster helpers (barrier.cluster + DSMEM)
 // ---------------------------------------------------------------------------
