@@ -91,6 +91,10 @@ static int fail(int code, const std::string& msg) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+#ifndef RHSEG_L2_PERSIST_MB
+#define RHSEG_L2_PERSIST_MB 64
+#endif
+
 // ---------------------------------------------------------------------------
 // one batch of sections (a quadtree level or a standalone graph)
 // ---------------------------------------------------------------------------
@@ -139,6 +143,7 @@ struct rhseg_ctx {
     // repeated runs of one shape allocate nothing, so no run waits on the driver.
     std::map<int, std::pair<void*, size_t>> bufs;
     size_t dmat_budget = 0;  // bytes the D matrix may use (measured once per ctx)
+    size_t l2_persist_bytes = 0;  // persisting-L2 set-aside granted at ctx creation
     // host-input pipeline (rhseg_run_host): a copy stream and per-chunk streams/events
     cudaStream_t copy_stream = nullptr;
     cudaStream_t pstream[8] = {};
@@ -284,6 +289,16 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.spec = spec ? 1 : 0;
     b.stage_bytes = stage_bytes;
     b.nstages = nstages;
+    // a level whose streamed means fit the persisting L2 set-aside keeps them there
+    b.l2_window_base = nullptr;
+    b.l2_window_bytes = 0;
+    if (spec && c->l2_persist_bytes > 0) {
+        const size_t mub = (size_t)(oSums - oMu);  // mu (+ mu2 / fp32 copies) are contiguous
+        if (mub <= c->l2_persist_bytes) {
+            b.l2_window_base = Wk + oMu;
+            b.l2_window_bytes = mub;
+        }
+    }
     b.measure = lv.measure;
     b.nrm2 = lv.measure == 2 ? reinterpret_cast<double*>(K + oN2) : nullptr;
     b.weight = weight;
@@ -437,6 +452,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
     unsigned long long ph[8] = {0};
     if (prof) CK(cudaMemcpyAsync(ph, prof, 8 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (lv.sb.l2_window_bytes) cudaCtxResetPersistingL2Cache();  // hand the set-aside back
     RHSEG_TRACE("run_level %d: synced", lv.level);
     if (prof) {
         long long steps = 0;
@@ -757,6 +773,15 @@ int rhseg_ctx_create(int device, rhseg_ctx** out) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    {   // persisting-L2 set-aside for small levels' streamed means (best effort)
+        int maxp = 0;
+        if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, device) == cudaSuccess && maxp > 0) {
+            const size_t want = std::min<size_t>((size_t)maxp, (size_t)RHSEG_L2_PERSIST_MB << 20);
+            if (want > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess)
+                c->l2_persist_bytes = want;
+        }
+        cudaGetLastError();
+    }
     *out = c;
     return RHSEG_OK;
 }

@@ -33,6 +33,8 @@ struct SectionBatch {
     int measure;   // 0 sqrt-bsmse (reference), 1 euclidean, 2 sam (extensions)
     int stage_bytes;  // merge-loop stream ring stage size (host-chosen)
     int nstages;      // merge-loop stream ring depth (host-chosen)
+    void* l2_window_base;    // L2-persisting access window of the loop launch (0 bytes = none)
+    size_t l2_window_bytes;
     double weight; // spectral_weight (engine.py:33)
     const int* R0;       // [nsec] initial live regions
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
