@@ -92,7 +92,7 @@ static int fail(int code, const std::string& msg) {
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 #ifndef RHSEG_L2_PERSIST_MB
-#define RHSEG_L2_PERSIST_MB 64
+#define RHSEG_L2_PERSIST_MB 0  // off: no gain on C2, C4 3% slower with a 64 MB set-aside
 #endif
 
 // ---------------------------------------------------------------------------
