@@ -383,3 +383,26 @@ def test_hseg_step_sequence_equals_hseg_run():
         steps.append((rec.survivor_id, rec.absorbed_id, rec.dissimilarity, int(rec.kind)))
     assert steps == [(r.survivor_id, r.absorbed_id, r.dissimilarity, int(r.kind)) for r in h.records]
     assert np.array_equal(g1.pixel_assignment, g2.pixel_assignment)
+
+
+@pytest.mark.parametrize("measure", ["sam", "sqrt-bsmse"])
+def test_config3_sampled_leaves_vs_oracle(measure, oracle):
+    """BASELINE config 3 at full size (512x512x224, L=5, w=0.21, t=16; SAM and its
+    BSMSE twin): the device run's logs for sampled leaves equal an independent
+    oracle HSEG of those leaves (leaves are independent sections)."""
+    img, _ = rh.gen_synthetic(512, 224, 16, 25, 3.0, 512)
+    res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(0.21, 16, measure), 5, 16))
+    logs = {(s.level, s.row, s.col): r for s, r in res.section_logs}
+    oracle.set_threads(os.cpu_count() or 1)
+    oracle.set_measure(measure)
+    try:
+        for (lr, lc) in ((0, 0), (9, 14)):
+            sub = np.ascontiguousarray(img.samples[:, 32 * lr:32 * lr + 32, 32 * lc:32 * lc + 32])
+            ref = oracle.rhseg_run(sub, 1, 0.21, 16)
+            a, b, d, k = logs[(5, lr, lc)].arrays()
+            assert np.array_equal(np.asarray(a), ref["log_survivor"])
+            assert np.array_equal(np.asarray(b), ref["log_absorbed"])
+            assert np.array_equal(np.asarray(d).view(np.uint64), ref["log_dissim"].view(np.uint64))
+            assert np.array_equal(np.asarray(k), ref["log_kind"])
+    finally:
+        oracle.set_measure("sqrt-bsmse")
