@@ -406,3 +406,23 @@ def test_config3_sampled_leaves_vs_oracle(measure, oracle):
             assert np.array_equal(np.asarray(k), ref["log_kind"])
     finally:
         oracle.set_measure("sqrt-bsmse")
+
+
+def test_config4_sampled_leaves_vs_oracle(oracle):
+    """BASELINE config 4 at full size (2048x2048x224, L=7, 4096 leaves, 4.19 M
+    merges) through the executor: sampled leaves equal the oracle bit for bit,
+    the merge count is the analytic one, labels are dense and the root holds 16
+    regions."""
+    img, _ = rh.gen_synthetic(2048, 224, 16, 25, 3.0, 2048)
+    res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(0.21, 16), 7, 16))
+    assert sum(len(r) for _, r in res.section_logs) == 4194288
+    assert res.labels.label_count() == 16 and res.graph.live_count == 16
+    logs = {(s.level, s.row, s.col): r for s, r in res.section_logs}
+    oracle.set_threads(os.cpu_count() or 1)
+    for (lr, lc) in ((0, 0), (37, 50)):
+        sub = np.ascontiguousarray(img.samples[:, 32 * lr:32 * lr + 32, 32 * lc:32 * lc + 32])
+        ref = oracle.rhseg_run(sub, 1, 0.21, 16)
+        a, b, d, k = logs[(7, lr, lc)].arrays()
+        assert np.array_equal(np.asarray(a), ref["log_survivor"])
+        assert np.array_equal(np.asarray(b), ref["log_absorbed"])
+        assert np.array_equal(np.asarray(d).view(np.uint64), ref["log_dissim"].view(np.uint64))
