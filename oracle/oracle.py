@@ -42,6 +42,8 @@ def lib():
         L.oracle_hseg_graph.restype = i64
         L.oracle_rhseg_run.argtypes = [vp, i64, i64, i32, f64, i64, i64, i32, i64] + [vp] * 11
         L.oracle_rhseg_run.restype = i64
+        L.oracle_rhseg_replay_leaves.argtypes = [vp, i64, i64, i32, f64, i64, i64, i32, i64] + [vp] * 16
+        L.oracle_rhseg_replay_leaves.restype = i64
         L.oracle_run_leaf.argtypes = [vp, i64, i64, i64, i64, i64, f64, i64, i32, i64]
         L.oracle_run_leaf.restype = i64
         L.oracle_set_threads.argtypes = [ctypes.c_int]
@@ -148,6 +150,49 @@ def rhseg_run(samples, levels, weight, target, section_target=None, connectivity
         int(connectivity), cap, _p(out["log_level"]), _p(out["log_row"]), _p(out["log_col"]),
         _p(out["log_survivor"]), _p(out["log_absorbed"]), _p(out["log_dissim"]),
         _p(out["log_kind"]), _p(labels), _p(assignment), _p(rootinit), _p(conv))
+    if n < 0:
+        raise ValueError(f"edge {edge} not divisible by {2 ** (levels - 1)} (levels={levels})")
+    res = {k: v[:n] for k, v in out.items()}
+    res["labels"] = labels.reshape(edge, edge)
+    res["assignment"] = assignment.reshape(edge, edge)
+    res["root_initial_count"] = int(rootinit[0])
+    res["converged_early"] = bool(conv[0])
+    return res
+
+
+def rhseg_replay_leaves(samples, levels, weight, target, section_target, leaf_logs, connectivity=8):
+    """rhseg_run with the leaf level REPLAYED from `leaf_logs` = (counts per leaf
+    row-major, survivor, absorbed, dissim, kind) and every upper level computed
+    from scratch (recursive.py:145-170): checks all upper levels of a run too big
+    for the from-scratch oracle. Returns the same dict as rhseg_run."""
+    samples = np.ascontiguousarray(samples, dtype=np.float32)
+    nb, edge, _ = samples.shape
+    counts, sv, ab, dd, kk = leaf_logs
+    counts = np.ascontiguousarray(counts, np.int64)
+    sv = np.ascontiguousarray(sv, np.int32)
+    ab = np.ascontiguousarray(ab, np.int32)
+    dd = np.ascontiguousarray(dd, np.float64)
+    kk = np.ascontiguousarray(kk, np.uint8)
+    cap = int(counts.sum()) + edge * edge + 16
+    out = {
+        "log_level": np.zeros(cap, np.int16),
+        "log_row": np.zeros(cap, np.int32),
+        "log_col": np.zeros(cap, np.int32),
+        "log_survivor": np.zeros(cap, np.int32),
+        "log_absorbed": np.zeros(cap, np.int32),
+        "log_dissim": np.zeros(cap, np.float64),
+        "log_kind": np.zeros(cap, np.uint8),
+    }
+    labels = np.zeros(edge * edge, np.int32)
+    assignment = np.zeros(edge * edge, np.int32)
+    rootinit = np.zeros(1, np.int64)
+    conv = np.zeros(1, np.int32)
+    n = lib().oracle_rhseg_replay_leaves(
+        _p(samples), edge, nb, int(levels), float(weight), int(target), int(section_target),
+        int(connectivity), cap, _p(out["log_level"]), _p(out["log_row"]), _p(out["log_col"]),
+        _p(out["log_survivor"]), _p(out["log_absorbed"]), _p(out["log_dissim"]),
+        _p(out["log_kind"]), _p(labels), _p(assignment), _p(rootinit), _p(conv),
+        _p(counts), _p(sv), _p(ab), _p(dd), _p(kk))
     if n < 0:
         raise ValueError(f"edge {edge} not divisible by {2 ** (levels - 1)} (levels={levels})")
     res = {k: v[:n] for k, v in out.items()}

@@ -404,8 +404,33 @@ def test_config3_sampled_leaves_vs_oracle(measure, oracle):
             assert np.array_equal(np.asarray(b), ref["log_absorbed"])
             assert np.array_equal(np.asarray(d).view(np.uint64), ref["log_dissim"].view(np.uint64))
             assert np.array_equal(np.asarray(k), ref["log_kind"])
+        _upper_levels_vs_replay(oracle, img, res, 5, 0.21, 16, 16)
     finally:
         oracle.set_measure("sqrt-bsmse")
+
+
+def _upper_levels_vs_replay(oracle, img, res, levels, w, t, st):
+    """Every level above the leaves: the oracle replays the device's leaf logs and
+    computes the upper levels from scratch; logs and labels must match."""
+    side = 1 << (levels - 1)
+    logs = {(s.level, s.row, s.col): r for s, r in res.section_logs}
+    cnt, parts = [], [[], [], [], []]
+    for r in range(side):
+        for c in range(side):
+            arr = logs[(levels, r, c)].arrays()
+            cnt.append(len(arr[0]))
+            for q in range(4):
+                parts[q].append(np.asarray(arr[q]))
+    leaf = (cnt, *[np.concatenate(p) for p in parts])
+    ref = oracle.rhseg_replay_leaves(img.samples, levels, w, t, st, leaf)
+    got = _flat(res)
+    for k in LOG_KEYS:
+        g, e = np.asarray(got[k]), np.asarray(ref[k])
+        if k == "log_dissim":
+            assert np.array_equal(g.view(np.uint64), e.view(np.uint64)), k
+        else:
+            assert np.array_equal(g.astype(np.int64), e.astype(np.int64)), k
+    assert np.array_equal(res.labels.labels, ref["labels"])
 
 
 def test_config4_sampled_leaves_vs_oracle(oracle):

@@ -118,3 +118,19 @@ def test_extension_measures_known_answers(oracle):
             assert d == fn(1, 1, [1.0, 2.0], [4.0, 6.0]), name
         else:
             assert d == math.sqrt(0.5 * 25.0)
+
+
+def test_oracle_replay_leaves_equals_full_run(oracle):
+    """The upper-level checker (leaves replayed from a log, levels above computed
+    from scratch) reproduces the full oracle run."""
+    from paper_2106_12942_b200 import gen_synthetic
+
+    img, _ = gen_synthetic(32, 6, 4, 6, 3.0, 5)
+    full = oracle.rhseg_run(img.samples, 3, 0.21, 4, 9)
+    m = full["log_level"] == 3
+    cnt = [int((m & (full["log_row"] == r) & (full["log_col"] == c)).sum()) for r in range(4) for c in range(4)]
+    rep = oracle.rhseg_replay_leaves(img.samples, 3, 0.21, 4, 9, (cnt, full["log_survivor"][m],
+                                     full["log_absorbed"][m], full["log_dissim"][m], full["log_kind"][m]))
+    for k, v in full.items():
+        if isinstance(v, np.ndarray):
+            assert np.array_equal(v, rep[k]), k
