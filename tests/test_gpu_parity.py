@@ -433,6 +433,15 @@ def _upper_levels_vs_replay(oracle, img, res, levels, w, t, st):
     assert np.array_equal(res.labels.labels, ref["labels"])
 
 
+def test_config4_upper_levels_vs_oracle(oracle):
+    """BASELINE config 4: all 1365 sections above the leaves (levels 1-6) and the
+    final labels, against the oracle replaying the device's 4096 leaf logs."""
+    img, _ = rh.gen_synthetic(2048, 224, 16, 25, 3.0, 2048)
+    res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(0.21, 16), 7, 16))
+    oracle.set_threads(os.cpu_count() or 1)
+    _upper_levels_vs_replay(oracle, img, res, 7, 0.21, 16, 16)
+
+
 def test_config4_sampled_leaves_vs_oracle(oracle):
     """BASELINE config 4 at full size (2048x2048x224, L=7, 4096 leaves, 4.19 M
     merges) through the executor: sampled leaves equal the oracle bit for bit,
