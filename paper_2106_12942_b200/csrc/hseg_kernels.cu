@@ -184,13 +184,8 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
 // per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
-#ifndef RHSEG_F32FILTER
-// Experimental (off): stream fp32 filter means with exact fp64 re-evaluation.
-// Bit-exact (the GPU suite passes with it on) but slower on C4 (loop 1028 vs
-// 877 ms): the exact re-evaluations it needs every step (argmin winners, offer
-// overlaps, multi-candidate rescans) sit on each CTA's serial step chain and
-// cost more than the halved stream saves. profiles/r01_loop_variants.md.
-#define RHSEG_F32FILTER 0
+#ifndef RHSEG_APO
+#define RHSEG_APO 1  // bound row a' from D (no mean stream) where possible; host may still disable
 #endif
 #ifndef RHSEG_COMPACT_K
 #define RHSEG_COMPACT_K 16  // compaction threshold: holes^2 >= K * S (K=16: C4 loop 874 -> 864 ms)
@@ -213,12 +208,12 @@ constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per merge
 
 struct LoopSmem {
-    size_t fref, fxa, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C) + 1) & ~1; }
-__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2, bool f32,
+__host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2,
                                                      int stage_bytes, int nstages) {
     const size_t Rs = (size_t)own_rows(Rp, C);
     LoopSmem L;
@@ -240,8 +235,6 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.cnt = o;   o = align16(o + (size_t)Rp * 4);
     L.col = o;   o = align16(o + (spec ? Rs * 2 : 0));      // int16: region ids < 16384
     L.slot_of = o; o = align16(o + (spec ? Rs * 2 : 0));
-    L.fref = o;  o = align16(o + (f32 ? (size_t)B * 4 : 0));  // F32: centring reference (fp32)
-    L.fxa = o;   o = align16(o + (f32 ? (size_t)B * 4 : 0));  // F32: a's centred fp32 mean
     L.bAd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
     L.bNd2 = o;  o = align16(o + (top2 ? Rs * 8 : 0));
     L.bAj2 = o;  o = align16(o + (top2 ? Rs * 4 : 0));
@@ -249,27 +242,29 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.cx = o;    o = align16(o + (top2 ? Rs : 0));
     L.nbl = o;   o = align16(o + kNbList * 2);  // b's neighbours during a merge
     L.sra = o;   o = align16(o + (size_t)(Rp / 32) * 4);  // a's new adjacency row (row-a pass)
+    L.sdv = o;   o = align16(o + (spec && nstages == 0 ? Rs * 16 : 0));  // APO: per-slot D values / bounds
+    L.apk = o;   o += 64;                                                  // APO: argmin keys, rule scratch
+    L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
     o = (o + 127) & ~size_t(127);
     L.ring = o;
-    o += spec ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;
+    o += spec && nstages > 0 ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;  // (APO: no ring)
     L.total = o;
     return L;
 }
 __host__ __device__ inline bool use_top2(bool spec, int C, int measure) { return spec && C == 1 && measure == kSam; }
-__host__ __device__ inline bool use_f32(bool spec, int C, int measure) {
-    return RHSEG_F32FILTER && spec && C == 1 && measure != kSam;
+__host__ __device__ inline bool apo_capable(bool spec, int C, int measure) {
+    return RHSEG_APO && spec && C == 1 && measure != kSam;
 }
 int hseg_loop_stage_bytes(bool spec, int C, int measure) {
     return use_top2(spec, C, measure) ? kStageBytesTop2 : kStageBytes;
 }
 size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes, int nstages) {
-    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), use_f32(spec, C, measure), stage_bytes,
-                            nstages)
+    return loop_smem_layout(Rp, C, B, spec, use_top2(spec, C, measure), stage_bytes, nstages)
         .total;
 }
 int hseg_loop_max_stages() { return kMaxStages; }
 int hseg_loop_default_stages() { return RHSEG_STAGES; }
-bool hseg_use_f32(bool spec, int C, int measure) { return use_f32(spec, C, measure); }
+bool hseg_apo_capable(bool spec, int C, int measure) { return apo_capable(spec, C, measure); }
 int hseg_loop_max_rows() { return kMaxSlots; }
 
 __device__ __forceinline__ void cache_offer(double& cd, int& cj, double d, int j) {
@@ -344,83 +339,154 @@ struct Top2Lists {
     uint8_t* cx;
 };
 
-// ---- F32 filter (w > 0, BSMSE/Euclidean, one CTA per section) ---------------
-// The stream carries x = fl32(mu - ref) (ref: the section's region-0 mean at loop
-// start) instead of the fp64 means: half the bytes. Every dissimilarity the
-// merge sequence depends on is still the exact fp64 reference value: the fp32
-// sum only yields a rigorous interval [dlo, dhi] around the reference's d, and
-// every comparison the interval cannot settle is re-evaluated exactly (one warp,
-// means from the region-major fp64 band sums). Interval derivation: with
-// N = ||x||_2 bounds, |e| <= u32'|x| per band, eta = u(N_a+N_j) + u64||t~||,
-// |s~ - S| <= g s~ + 2 eta sqrt(s~) + eta^2 (g = (2B+16) u64 covers the fp64
-// accumulation of s~ and of the reference's own s), then directed-rounding
-// sqrt(coef * s_lo/hi) with a final (1 -/+ 8e-16).
-template <int M>
-__device__ __forceinline__ void f32_interval(double st, double nsum, double ni, double nj, int B, double& dlo,
-                                             double& dhi) {
-    const double u = 5.97e-8;                                  // 2^-24 (1 + 1.6e-3)
-    const double g = (2.0 * B + 16.0) * 1.1102230246251565e-16;  // fp64 accumulation
-    const double rt = sqrt(st);
-    const double eta = u * nsum + 1.2e-16 * rt + 1e-43;
-    double err = g * st + 2.0 * eta * rt + eta * eta;
-    err = (err + g * (st + err)) * 1.01;
-    const double slo = fmax(0.0, st - err), shi = st + err;
-    if (M == kBsmse) {
-        const double coef = __ddiv_rn(__dmul_rn(ni, nj), __dadd_rn(ni, nj));
-        dlo = __dsqrt_rd(__dmul_rd(coef, slo)) * (1.0 - 8e-16);
-        dhi = __dsqrt_ru(__dmul_ru(coef, shi)) * (1.0 + 8e-16);
-    } else {
-        dlo = __dsqrt_rd(slo) * (1.0 - 8e-16);
-        dhi = __dsqrt_ru(shi) * (1.0 + 8e-16);
-    }
-}
-// D entries: exact values are >= 0 doubles; an interval is stored as
-// [sign=1 | float(dlo) rounded down | float(dhi) rounded up].
-__device__ __forceinline__ double d_pack_interval(double dlo, double dhi) {
-    const unsigned long long lo = __float_as_uint(__double2float_rd(dlo));
-    const unsigned long long hi = __float_as_uint(__double2float_ru(dhi));
-    return __longlong_as_double((long long)((1ULL << 63) | (lo << 32) | hi));
-}
+// ---- APO: row a' without the mean stream (w > 0, BSMSE/Euclidean, one CTA per section)
+// After merging b into a, the new mean is m' = lam m_a + (1 - lam) m_b + e (lam = n_a/n,
+// e = the rounding of the new sums / count), and for every region j the parallelogram
+// identity gives, exactly in real arithmetic,
+//     || lam m_a + (1-lam) m_b - m_j ||^2 = lam T_aj + (1-lam) T_bj - lam (1-lam) T_ab
+// with T_xy = ||m_x - m_y||^2. D already holds d(a, j), d(b, j) and d(a, b), and the
+// reference value satisfies d^2 = C T (1 + eps) with |eps| <= E = (B + 8) u (C = n_x n_y /
+// (n_x + n_y) for BSMSE, 1 for Euclidean: ascending-band sum of B rounded squares, the
+// coefficient product, sqrt). So two D rows (16 bytes per column instead of the 8B + 16
+// bytes of a mean column) give a rigorous interval around the reference's d(a', j):
+// directed-rounding arithmetic throughout, ||e|| <= 3.01 u max ||m|| (max over the
+// section's initial means, which bound every later mean). Entries the interval cannot
+// settle are evaluated exactly (warp_exact) -- offers that may beat a row's cached best
+// (0.3 per step on a C4 leaf), a's best when several columns tie within their intervals,
+// argmin winners, multi-candidate rescans -- so every dissimilarity the merge sequence
+// and the log see is the reference's exact fp64 value.
+//
+// D entries: an exact value is a non-negative double (sign bit clear). An interval is
+// [sign=1 | centre c with its low 6 mantissa bits replaced by k] = c (1 -/+ 2^(k-46)),
+// decoded with directed multiplies (single DMUL.RM/.RP instructions).
+//
+// The interval arithmetic itself is round-to-nearest with explicit slack (directed
+// division/sqrt are long software sequences): with u = 2^-53, every quantity below is
+// within a few u of its real value, and each bound is widened by at least twice the
+// worst-case accumulated error:
+//   A = d(a,j)^2 (1/n_a + 1/n_j) = T_aj (1 + eps) (1 +- 5u)        (d^2 = C T (1 + eps))
+//   V = lam A + (1-lam) B - lam(1-lam) T_ab,  |V - V_true| <= (E + 12u) S,  S = sum of |terms|
+//   ||v|| in [sqrt(V_lo - 2(E+16u)S), sqrt(V_hi + 2(E+16u)S)]   (the rounding of the
+//        subtraction and sqrt is covered by the doubled slack; ||v|| <= 2 max||m||)
+//   sqrt(T') in [||v|| -+ ee], ee = 10u max||m|| (>= 3.02u max||m|| for e, + sqrt/sub rounding)
+//   d(a',j) = sqrt(C') sqrt(T') sqrt(1 + eps'),  widened by 2 (E/2 + 8u) relative.
+constexpr double kU64 = 1.1102230246251565e-16;
+constexpr int kApoKMax = 45;  // widest encodable interval: c (1 -/+ 1/2)
 __device__ __forceinline__ bool d_is_interval(double v) { return __double_as_longlong(v) < 0; }
-__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    if ((long long)b < 0) {
-        lo = (double)__uint_as_float((uint32_t)(b >> 32) & 0x7fffffffu);
-        hi = (double)__uint_as_float((uint32_t)b);
-    } else {
-        lo = hi = v;
-    }
+__device__ __forceinline__ void d_decode(double c, int k, double& lo, double& hi) {
+    const double rho = __longlong_as_double((long long)(k - 46 + 1023) << 52);
+    lo = __dmul_rd(c, 1.0 - rho);  // 1 -/+ rho are exact for 2^-46 <= rho <= 1/2
+    hi = __dmul_ru(c, 1.0 + rho);
 }
-// Exact d(i, j) by one warp (all lanes return it): means from the region-major
-// fp64 band sums (sums[r][k] / count[r], the exact cached values), or from an
-// fp64 mean vector in shared memory; ascending-band accumulation via shuffles.
+__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
+    const long long b = __double_as_longlong(v);
+    if (b < 0) d_decode(__longlong_as_double(b & 0x7fffffffffffffc0LL), (int)(b & 63), lo, hi);
+    else lo = hi = v;
+}
+// encode [lo, hi] (0 < lo <= hi < inf); false when the interval is too wide to encode
+__device__ __forceinline__ bool d_pack_interval(double lo, double hi, double& out) {
+    if (lo == hi) { out = lo; return true; }
+    if (!(lo > 0.0) || !(hi < kInf)) return false;
+    const long long cb = __double_as_longlong(0.5 * lo + 0.5 * hi) & 0x7fffffffffffffc0LL;
+    const double c = __longlong_as_double(cb);  // truncated centre
+    // first guess from the exponents of the half-width and the centre, then verify
+    // with the decoder itself (rarely more than one extra iteration)
+    const double w = fmax(hi - c, c - lo);
+    const int ew = (int)((__double_as_longlong(w) >> 52) & 0x7ff), ec = (int)((cb >> 52) & 0x7ff);
+    int k = max(0, ew - ec + 47);
+    for (; k <= kApoKMax; ++k) {
+        double l2, h2;
+        d_decode(c, k, l2, h2);
+        if (l2 <= lo && h2 >= hi) break;
+    }
+    if (k > kApoKMax) return false;
+    out = __longlong_as_double((long long)(0x8000000000000000ULL | (unsigned long long)cb | (unsigned long long)k));
+    return true;
+}
+// Per-step constants of the row-a' pass (identical in every thread).
+struct ApoStep {
+    double lam, mu, kt_lo, kt_hi;  // na/nn, nb/nn, lam mu T_ab (d(a, b) may be an interval)
+    double rna, rnb, rnn;
+    double vslack, ee, mrel;
+};
 template <int M>
-__device__ __forceinline__ double warp_exact(const double* mi_smem, const double* si, double ci, const double* sj,
-                                             double cj, int B, int lane) {
-    // the per-band terms are independent (all lanes in parallel); only the
-    // ascending-band sum is a serial chain, fed by shuffles issued ahead of it
+__device__ __forceinline__ ApoStep apo_step(double na, double nb, double dab, double E, double ee) {
+    ApoStep p;
+    const double nn = na + nb;
+    p.lam = na / nn;
+    p.mu = nb / nn;
+    p.rna = M == kBsmse ? 1.0 / na : 0.0;
+    p.rnb = M == kBsmse ? 1.0 / nb : 0.0;
+    p.rnn = M == kBsmse ? 1.0 / nn : 0.0;
+    double dl, dh;
+    d_unpack(dab, dl, dh);
+    const double cab = M == kBsmse ? p.rna + p.rnb : 1.0;
+    p.kt_lo = p.lam * p.mu * (dl * dl * cab);
+    p.kt_hi = p.lam * p.mu * (dh * dh * cab);
+    p.vslack = 2.0 * (E + 16.0 * kU64);
+    p.ee = ee;
+    p.mrel = 2.0 * (0.5 * E + 8.0 * kU64);
+    return p;
+}
+// interval around the reference's d(a', j) from the raw D entries d(a, j), d(b, j)
+template <int M>
+__device__ __forceinline__ void apo_interval(const ApoStep& p, double rA, double rB, double nj, double& dlo,
+                                             double& dhi) {
+    double al, ah, bl, bh;
+    d_unpack(rA, al, ah);
+    d_unpack(rB, bl, bh);
+    const double rj = M == kBsmse ? 1.0 / nj : 0.0;
+    const double ca = M == kBsmse ? p.rna + rj : 1.0, cb = M == kBsmse ? p.rnb + rj : 1.0;
+    const double Al = al * al * ca, Ah = ah * ah * ca, Bl = bl * bl * cb, Bh = bh * bh * cb;
+    const double Vl = p.lam * Al + p.mu * Bl - p.kt_hi;
+    const double Vh = p.lam * Ah + p.mu * Bh - p.kt_lo;
+    const double dv = p.vslack * (p.lam * Ah + p.mu * Bh + p.kt_hi);
+    const double nlo = fmax(0.0, sqrt(fmax(0.0, Vl - dv)) - p.ee);
+    const double nhi = sqrt(fmax(0.0, Vh + dv)) + p.ee;
+    const double sc = M == kBsmse ? sqrt(1.0 / (p.rnn + rj)) : 1.0;  // sqrt(C')
+    dlo = nlo * sc * (1.0 - p.mrel);
+    dhi = nhi * sc * (1.0 + p.mrel);
+}
+
+// Exact d(i, j) by one warp (all lanes return it) from two fp64 mean vectors
+// (shared or global memory; APO keeps a region-major copy of the exact cached means):
+// every lane loads its bands up front, the per-band terms are independent, and only
+// the ascending-band sum is a serial chain, fed by shuffles issued ahead of it.
+template <int M>
+__device__ __noinline__ double warp_exact(const double* mi, const double* mj, double ci, double cj, int B,
+                                             int lane) {
     double s = 0.0;
-    for (int k0 = 0; k0 < B; k0 += 32) {
-        const int k = k0 + lane;
-        double term = 0.0;
-        if (k < B) {
-            const double vi = mi_smem ? mi_smem[k] : __ddiv_rn(si[k], ci);
-            const double vj = __ddiv_rn(sj[k], cj);
+    for (int k0 = 0; k0 < B; k0 += 256) {
+        double term[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 32 * u + lane;
+            const double vi = k < B ? mi[k] : 0.0, vj = k < B ? __ldcg(mj + k) : 0.0;
             if (M == kSam) {
-                term = __dmul_rn(vi, vj);
+                term[u] = __dmul_rn(vi, vj);
             } else {
                 const double t = __dsub_rn(vi, vj);
-                term = __dmul_rn(t, t);
+                term[u] = __dmul_rn(t, t);
             }
         }
-        const int kn = min(32, B - k0);
 #pragma unroll
-        for (int kk = 0; kk < 32; ++kk) {
-            const double tk = __shfl_sync(0xffffffffu, term, kk);
-            if (kk < kn) s = __dadd_rn(s, tk);
+        for (int u = 0; u < 8; ++u) {
+            const int kn = min(32, B - (k0 + 32 * u));
+            if (kn <= 0) break;
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+                const double tk = __shfl_sync(0xffffffffu, term[u], kk);
+                if (kk < kn) s = __dadd_rn(s, tk);
+            }
         }
     }
     return pair_finish<M>(ci, cj, s, 0.0, 0.0);
+}
+
+// APO: a's best when its single candidate may be an interval (nothing to compare)
+__device__ __forceinline__ void rb_offer_iv(RowBest& b, double v, int j) {
+    if (__double_as_longlong(v) < 0) { b.d = v; b.j = j; }
+    else rb_offer(b, v, j);
 }
 
 // Epilogue for one column j of the row-a pass: D row/column update, offer
@@ -466,7 +532,7 @@ struct StreamState {
 #ifndef RHSEG_MINBLOCKS
 #define RHSEG_MINBLOCKS 2
 #endif
-template <bool CLUSTER, bool SPEC, int M>
+template <bool CLUSTER, bool SPEC, int M, bool APO = false>
 __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
     const long long t_entry = clock64();
@@ -481,12 +547,14 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
 
     constexpr bool TOP2 = SPEC && !CLUSTER && M == kSam;
-    constexpr bool F32 = RHSEG_F32FILTER && SPEC && !CLUSTER && M != kSam;
-    using SE = typename std::conditional<F32, float, double>::type;  // streamed element
+    static_assert(!APO || (SPEC && !CLUSTER && M != kSam), "APO: w > 0, one CTA, BSMSE/Euclidean");
+    constexpr bool F32 = APO;  // interval-valued D entries and caches (resolved exactly on demand)
+    constexpr bool STREAM = SPEC && !APO;  // row a' from the streamed mean columns
+    using SE = double;  // streamed element
     constexpr int ES = (int)sizeof(SE);
     const int SB = bt.stage_bytes;  // ring stage size and depth chosen by the host
     const int NS = bt.nstages;      // (deeper ring when the level has <= 1 CTA per SM)
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, F32, SB, NS);
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, SB, NS);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -508,8 +576,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
     short* col = reinterpret_cast<short*>(smem + L.col);
     short* slot_of = reinterpret_cast<short*>(smem + L.slot_of);
-    float* fref = reinterpret_cast<float*>(smem + L.fref);
-    float* fxa = reinterpret_cast<float*>(smem + L.fxa);
     // TOP2: second-best partner per row and stage + "list holds every candidate" bits
     double* bAd2 = reinterpret_cast<double*>(smem + L.bAd2);
     double* bNd2 = reinterpret_cast<double*>(smem + L.bNd2);
@@ -522,10 +588,15 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
     double* const mu0 = bt.mu + sec * bt.mu_stride();
-    double* const mu1 = (SPEC && !F32) ? bt.mu2 + sec * bt.mu_stride() : nullptr;
-    // the streamed mean buffers: fp64 mu / mu2, or the centred fp32 copies (F32)
-    SE* const sb0 = reinterpret_cast<SE*>(F32 ? (void*)(bt.mu32 + sec * bt.mu_stride()) : (void*)mu0);
-    SE* const sb1 = reinterpret_cast<SE*>(F32 ? (void*)(bt.mu32b + sec * bt.mu_stride()) : (void*)mu1);
+    double* const mu1 = STREAM ? bt.mu2 + sec * bt.mu_stride() : nullptr;
+    SE* const sb0 = mu0;  // the streamed mean buffers (ping-pong)
+    SE* const sb1 = mu1;
+    // APO: region-major copy of the exact cached means [Rp][B] (in the mu2 allocation)
+    // APO: versioned region-major means [2 Rp][B] (row i: initial mean of region i; row
+    // R0 + t: the mean created by step t) -- the exact re-evaluations read them, and
+    // the log's exact values are computed after the loop from (old a, b) versions
+    double* const mr = APO ? bt.mu2 + 2 * sec * bt.mu_stride() : nullptr;
+    unsigned short* ver = reinterpret_cast<unsigned short*>(smem + L.ver);  // APO: region -> mr row
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
@@ -611,12 +682,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
     };
 
-    // F32 rescan: D rows hold exact values and intervals; the row's best may be
-    // cached as an interval. One pass finds, per stage, the smallest upper bound U
-    // and the two smallest lower bounds: if the second lies above U the entry with
-    // the smallest lower bound is the row's minimum (cached as it is); otherwise a
-    // second pass takes the exact lexicographic minimum of every entry whose
-    // lower bound reaches U (intervals evaluated by the warp, written back to D).
+    // APO rescan: D rows hold exact values and intervals, and so may the cached best.
+    // One pass finds, per stage, the smallest upper bound U and the two smallest
+    // lower bounds: if the second lies above U, the entry with the smallest lower
+    // bound is the row's minimum (cached as it is, interval or not); otherwise
+    // a second pass takes the exact lexicographic minimum of every entry whose lower
+    // bound reaches U (intervals evaluated by the warp and written back to D).
     struct Lo2 {
         double l1, v1, l2, u;
         int j1;
@@ -628,6 +699,19 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         } else if (l < x.l2) {
             x.l2 = l;
         }
+    };
+    auto exact_pair = [&](int i, int j) {  // whole warp; lane 0 writes D back
+        const long long t0 = clock64();
+        const double d = warp_exact<M>(mr + (size_t)ver[i] * B, mr + (size_t)ver[j] * B, (double)cnt[i], (double)cnt[j], B, lane);
+        if (bt.prof && lane == 0) {
+            atomicAdd(bt.prof + 11, 1ull);
+            atomicAdd(bt.prof + 12, (unsigned long long)(clock64() - t0));
+        }
+        if (lane == 0) {
+            D[(size_t)i * Rp + j] = d;
+            D[(size_t)j * Rp + i] = d;
+        }
+        return d;
     };
     auto rescanf = [&](int i, int mask, int ex) {
         const uint32_t* arow = adj + (size_t)i * W;
@@ -678,8 +762,6 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (live_i && (multA || multN)) {
             if (multA) ba = rb_none();
             if (multN) bn = rb_none();
-            const double* si = sums + (size_t)i * B;
-            const double ci = (double)cnt[i];
             for (int s0 = 0; s0 < ss.S; s0 += 32) {
                 const int sl = s0 + lane;
                 const int j = sl < ss.S ? col[sl] : -1;
@@ -704,11 +786,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     m &= m - 1;
                     const int jj = __shfl_sync(0xffffffffu, j, src);
                     const bool ajj = __shfl_sync(0xffffffffu, aj, src);
-                    const double d = warp_exact<M>(nullptr, si, ci, sums + (size_t)jj * B, (double)cnt[jj], B, lane);
-                    if (lane == 0) {
-                        drow[jj] = d;
-                        D[(size_t)jj * Rp + i] = d;
-                    }
+                    const double d = exact_pair(i, jj);
                     if (lane == src) {
                         if (ajj) rb_offer(ba, d, jj);
                         else rb_offer(bn, d, jj);
@@ -826,15 +904,17 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             const SE* src = (ss.cur ? sb1 : sb0) + lo + s;
             SE* dst = (ss.cur ? sb0 : sb1) + lo + np;
             if (id >= 0) {
+                if (STREAM) {
 #pragma unroll 8
-                for (int k = 0; k < B; ++k) dst[(size_t)k * Rp] = src[(size_t)k * Rp];
+                    for (int k = 0; k < B; ++k) dst[(size_t)k * Rp] = src[(size_t)k * Rp];
+                }
                 slot_of[id - lo] = np;
             }
             __syncthreads();  // every read of col[] in this chunk precedes the writes below
             if (id >= 0) col[np] = id;
             base += tot;
         }
-        fence_proxy_async_global();
+        if (STREAM) fence_proxy_async_global();
         __syncthreads();
         ss.S = base;
         ss.holes = 0;
@@ -846,6 +926,10 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     auto begin_stream = [&]() {
         // compact when holes >= 2 sqrt(S): balances the streamed holes (~1/sqrt(S) of
         // the bytes) against the copy cost (2 S B words every 2 sqrt(S) merges)
+        if (!STREAM) {  // APO: only the column list (no mean columns) is compacted
+            if (ss.S >= 64 && ss.holes * 8 >= ss.S) compact();
+            return;
+        }
         if (ss.S >= 64 && ss.holes * ss.holes >= RHSEG_COMPACT_K * ss.S) compact();
         constexpr int kAlign = 16 / ES;  // bulk copies move multiples of 16 bytes
         ss.S2 = (ss.S + kAlign - 1) / kAlign * kAlign;
@@ -866,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             slot_of[r] = r;
         }
         ss.S = max(0, hi - lo);
-        if (tid == 0)
+        if (STREAM && tid == 0)
             for (int s = 0; s < NS; ++s) {
                 mbar_init(&bars[s], 1);
             }
@@ -881,21 +965,31 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         rpart[1] = rb_none();
     }
     __syncthreads();
-    if (F32) {
-        // centre on region 0's mean (rounded to fp32), fp32 stream copy + norm bounds
-        for (int k = tid; k < B; k += kThreads) fref[k] = __double2float_rn(mu0[(size_t)k * Rp]);
+    double apoE = 0.0, apoEe = 0.0;
+    if (APO) {
+        // ||m|| bound for the whole loop: every later mean is a weighted average of the
+        // initial ones (times (1 + u)^depth), so per band max_i |m_i[k]| bounds |m[k]|
+        double* sx = reinterpret_cast<double*>(misc + 8);
+        if (tid == 0) *sx = 0.0;
         __syncthreads();
-        for (int sl = tid; sl < hi - lo; sl += kThreads) {
-            const int j = lo + sl;
-            double nrm = 0.0;
-            for (int k = 0; k < B; ++k) {
-                const float x = __double2float_rn(__dsub_rn(mu0[(size_t)k * Rp + j], (double)fref[k]));
-                sb0[(size_t)k * Rp + j] = (SE)x;
-                nrm += (double)x * (double)x;
-            }
-            bt.xnorm[(size_t)sec * Rp + j] = sqrt(nrm) * (1.0 + 1e-6) + 1e-300;
+        double acc = 0.0;
+        for (int k = warp; k < B; k += kWarps) {
+            double mx = 0.0;
+            for (int i = lane; i < R0; i += 32)
+                if (cnt[i] != 0u) mx = fmax(mx, fabs(mu0[(size_t)k * Rp + i]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            acc = __dadd_ru(acc, __dmul_ru(mx, mx));
         }
-        fence_proxy_async_global();
+        if (lane == 0) atomicAdd(sx, acc);  // (any order: rounded up afterwards)
+        __syncthreads();
+        apoE = (double)(B + 8) * kU64 * 1.01;
+        for (size_t e = tid; e < (size_t)R0 * B; e += kThreads) {
+            const int i = (int)(e / B);
+            if (cnt[i] != 0u) mr[e] = __ddiv_rn(sums[e], (double)cnt[i]);  // == the cached mean, bit for bit
+        }
+        for (int i = tid; i < Rp; i += kThreads) ver[i] = (unsigned short)i;
+        apoEe = sqrt(*sx * (1.0 + 1e-9)) * (10.0 * kU64 * 1.01);  // see apo_interval
         __syncthreads();
     }
     if (TOP2) {
@@ -923,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     int a_prev = -1, step = 0, conv = 0;
     long long pairs = 0;
     // optional per-phase cycle accounting (RHSEG_PROFILE=1): thread 0 of every CTA
-    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // (+ APO counters at prof[8..15])
     long long tmark = clock64();
     pc[6] = (unsigned long long)(tmark - t_entry);  // prologue (caches, initial rescans, E)
     auto mark = [&](int ph) {
@@ -939,11 +1033,14 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         // previous step (or in the prologue); columns a and b of this step are never
         // read from it.
         // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
-        Pair ca = pair_none(), cn = pair_none();
-        if (F32) {
-            // row caches may hold intervals: the stage minimum is among the rows whose
-            // lower bound reaches below the smallest upper bound; those are made
-            // exact (warps), then the usual lexicographic (d, min id, max id) pick
+        Pair A = pair_none(), N = pair_none();
+        RowBest PA = rb_none(), PN = rb_none();
+        unsigned* ak = reinterpret_cast<unsigned*>(smem + L.apk);  // APO: [0..1] min key, [2..3] max key, [4..5] min row
+        if (APO) {
+            // row caches may hold intervals. Per stage, the minimum lies among the rows
+            // whose lower bound reaches the smallest upper bound; when those rows all
+            // hold the same pair (typically rows i and j of the winning pair) it is the
+            // winner, interval or not. Otherwise their intervals are made exact.
             if (tid == 0) {
                 if (a_prev >= 0) {
                     const int r = a_prev - lo;
@@ -955,6 +1052,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 ninv = 0;
                 nnb = 0;
                 sScan = 0;
+                ak[0] = ak[1] = ak[4] = ak[5] = 0xffffffffu;
+                ak[2] = ak[3] = 0u;
             }
             __syncthreads();
             double uA = kInf, uN = kInf;
@@ -975,40 +1074,62 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             for (int i = lo + tid; i < hi; i += kThreads) {
                 if (cnt[i] == 0u) continue;
                 const int r = i - lo;
-                double l2, h2;
-                if (bAj[r] >= 0) {
-                    d_unpack(bAd[r], l2, h2);
-                    if (l2 <= uA) clist[atomicAdd(&sScan, 1)] = (unsigned short)i;
-                }
-                if (bNj[r] >= 0) {
-                    d_unpack(bNd[r], l2, h2);
-                    if (l2 <= uN) clist[atomicAdd(&sScan, 1)] = (unsigned short)(i | 0x4000);
-                }
-            }
-            __syncthreads();
-            const int nc = sScan;
-            for (int t = warp; t < nc; t += kWarps) {
-                const int e = clist[t], i = e & 0x3fff, st = e >> 14, r = i - lo;
-                const int j = st ? bNj[r] : bAj[r];
-                const double v = st ? bNd[r] : bAd[r];
-                if (!d_is_interval(v)) continue;
-                const double d = warp_exact<M>(nullptr, sums + (size_t)i * B, (double)cnt[i], sums + (size_t)j * B,
-                                               (double)cnt[j], B, lane);
-                if (lane == 0) {
-                    if (st) bNd[r] = d;
-                    else bAd[r] = d;
-                    D[(size_t)i * Rp + j] = d;
-                    D[(size_t)j * Rp + i] = d;
+#pragma unroll
+                for (int st = 0; st < 2; ++st) {
+                    const int j = st ? bNj[r] : bAj[r];
+                    if (j < 0) continue;
+                    double l2, h2;
+                    d_unpack(st ? bNd[r] : bAd[r], l2, h2);
+                    if (!(l2 <= (st ? uN : uA))) continue;
+                    const unsigned key = ((unsigned)min(i, j) << 16) | (unsigned)max(i, j);
+                    atomicMin(&ak[st], key);
+                    atomicMax(&ak[2 + st], key);
+                    atomicMin(&ak[4 + st], (unsigned)i);
+                    clist[atomicAdd(&sScan, 1)] = (unsigned short)(i | (st << 14));
                 }
             }
             __syncthreads();
-            for (int t = tid; t < nc; t += kThreads) {
-                const int e = clist[t], i = e & 0x3fff, r = i - lo;
-                if (e >> 14) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
-                else pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
+            const bool hasCA = ak[4] != 0xffffffffu, hasCN = ak[5] != 0xffffffffu;
+            const bool multA = hasCA && ak[0] != ak[2], multN = hasCN && ak[1] != ak[3];
+            if (multA || multN) {  // distinct pairs within each other's intervals (ties)
+                const int nc = sScan;
+                for (int t = warp; t < nc; t += kWarps) {
+                    const int e = clist[t], i = e & 0x3fff, st = e >> 14, r = i - lo;
+                    if (!(st ? multN : multA)) continue;
+                    const int j = st ? bNj[r] : bAj[r];
+                    if (!d_is_interval(st ? bNd[r] : bAd[r])) continue;
+                    const double d = exact_pair(i, j);
+                    if (lane == 0) {
+                        if (st) bNd[r] = d;
+                        else bAd[r] = d;
+                    }
+                }
+                __syncthreads();
+                Pair ca = pair_none(), cn = pair_none();
+                for (int t = tid; t < nc; t += kThreads) {
+                    const int e = clist[t], i = e & 0x3fff, r = i - lo;
+                    if (e >> 14) {
+                        if (multN) pair_offer(cn, make_pair(bNd[r], i, bNj[r]));
+                    } else if (multA) {
+                        pair_offer(ca, make_pair(bAd[r], i, bAj[r]));
+                    }
+                }
+                block_min_pair2(ca, cn, pscr);
+                if (multA) A = ca;
+                if (multN) N = cn;
             }
-            block_min_pair2(ca, cn, pscr);
+            if (hasCA && !multA) {
+                const int i = (int)ak[4], r = i - lo;
+                A = make_pair(bAd[r], i, bAj[r]);
+            }
+            if (hasCN && !multN) {
+                const int i = (int)ak[5], r = i - lo;
+                N = make_pair(bNd[r], i, bNj[r]);
+            }
+            mark(0);
         } else {
+            // (A) best pair over this CTA's rows (engine.py:281-296 restricted to own rows)
+            Pair ca = pair_none(), cn = pair_none();
             for (int i = lo + tid; i < hi; i += kThreads) {
                 if (cnt[i] == 0u || i == a_prev) continue;
                 const int r = i - lo;
@@ -1018,53 +1139,51 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (tid == 0) { ninv = 0; nnb = 0; }
             if (SPEC) block_min_pair2(ca, cn, pscr);
             else ca = block_min_pair(ca, pscr);
-        }
-        if (tid == 0) {
-            slot[par].selA = ca;
-            slot[par].selN = cn;
-            slot[par].rpA = rpart[0];
-            slot[par].rpN = rpart[1];
-        }
-        if (CLUSTER) {
-            // push this CTA's slot into rslot[par][rank] of every CTA of the cluster
-            // (fire-and-forget DSMEM stores); after the release/acquire cluster
-            // barrier every CTA combines the C slots from its own shared memory
-            __syncthreads();
-            if (tid < C * 16) {
-                const int r = tid >> 4, w = tid & 15;
-                const uint32_t v = reinterpret_cast<const uint32_t*>(&slot[par])[w];
-                dsmem_st_u32(dsmem_addr(&rslot[par * kMaxCluster + rank], (unsigned)r) + 4u * w, v);
+            if (tid == 0) {
+                slot[par].selA = ca;
+                slot[par].selN = cn;
+                slot[par].rpA = rpart[0];
+                slot[par].rpN = rpart[1];
             }
-            cluster_barrier();
-        } else {
-            __syncthreads();
-        }
+            if (CLUSTER) {
+                // push this CTA's slot into rslot[par][rank] of every CTA of the cluster
+                // (fire-and-forget DSMEM stores); after the release/acquire cluster
+                // barrier every CTA combines the C slots from its own shared memory
+                __syncthreads();
+                if (tid < C * 16) {
+                    const int r = tid >> 4, w = tid & 15;
+                    const uint32_t v = reinterpret_cast<const uint32_t*>(&slot[par])[w];
+                    dsmem_st_u32(dsmem_addr(&rslot[par * kMaxCluster + rank], (unsigned)r) + 4u * w, v);
+                }
+                cluster_barrier();
+            } else {
+                __syncthreads();
+            }
 
-        mark(0);
-        // (B) combine the C slots: identical decision in every CTA
-        Pair A = pair_none(), N = pair_none();
-        RowBest PA = rb_none(), PN = rb_none();
-        for (int r = 0; r < C; ++r) {
-            const Slot& s = CLUSTER ? rslot[par * kMaxCluster + r] : slot[par];
-            pair_offer(A, s.selA);
-            rb_offer(PA, s.rpA.d, s.rpA.j);
-            if (SPEC) {
-                pair_offer(N, s.selN);
-                rb_offer(PN, s.rpN.d, s.rpN.j);
+            mark(0);
+            // (B) combine the C slots: identical decision in every CTA
+            for (int r = 0; r < C; ++r) {
+                const Slot& s = CLUSTER ? rslot[par * kMaxCluster + r] : slot[par];
+                pair_offer(A, s.selA);
+                rb_offer(PA, s.rpA.d, s.rpA.j);
+                if (SPEC) {
+                    pair_offer(N, s.selN);
+                    rb_offer(PN, s.rpN.d, s.rpN.j);
+                }
             }
-        }
-        if (a_prev >= 0 && !F32) {  // (F32: a_prev's row joined the candidates above)
-            if (PA.j != kNoJ) pair_offer(A, make_pair(PA.d, a_prev, PA.j));
-            if (SPEC && PN.j != kNoJ) pair_offer(N, make_pair(PN.d, a_prev, PN.j));
-            if (tid == 0 && a_prev >= lo && a_prev < hi) {
-                const int r = a_prev - lo;
-                bAd[r] = PA.d;
-                bAj[r] = PA.j == kNoJ ? -1 : PA.j;
-                if (SPEC) { bNd[r] = PN.d; bNj[r] = PN.j == kNoJ ? -1 : PN.j; }
-                if (TOP2) {  // a's fresh row: its best only (complete iff it has none)
-                    bAd2[r] = kInf; bAj2[r] = -1;
-                    bNd2[r] = kInf; bNj2[r] = -1;
-                    cx[r] = (uint8_t)((PA.j == kNoJ ? 1 : 0) | (PN.j == kNoJ ? 2 : 0));
+            if (a_prev >= 0) {
+                if (PA.j != kNoJ) pair_offer(A, make_pair(PA.d, a_prev, PA.j));
+                if (SPEC && PN.j != kNoJ) pair_offer(N, make_pair(PN.d, a_prev, PN.j));
+                if (tid == 0 && a_prev >= lo && a_prev < hi) {
+                    const int r = a_prev - lo;
+                    bAd[r] = PA.d;
+                    bAj[r] = PA.j == kNoJ ? -1 : PA.j;
+                    if (SPEC) { bNd[r] = PN.d; bNj[r] = PN.j == kNoJ ? -1 : PN.j; }
+                    if (TOP2) {  // a's fresh row: its best only (complete iff it has none)
+                        bAd2[r] = kInf; bAj2[r] = -1;
+                        bNd2[r] = kInf; bNj2[r] = -1;
+                        cx[r] = (uint8_t)((PA.j == kNoJ ? 1 : 0) | (PN.j == kNoJ ? 2 : 0));
+                    }
                 }
             }
         }
@@ -1073,13 +1192,37 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         double dch = 0.0;
         const bool hasA = A.hi != kNoJ;
         if (SPEC && N.hi != kNoJ) {
-            const double da = hasA ? A.d : kInf;
-            if (N.d < __dmul_rn(bt.weight, da)) { a = N.lo; b = N.hi; dch = N.d; kind = 1; }
+            if (APO) {
+                // decide on the intervals (rounding w * d_a is monotone); when they
+                // cannot, both dissimilarities are made exact (warps 0 and 1)
+                double nl, nh, al = kInf, ah = kInf;
+                d_unpack(N.d, nl, nh);
+                if (hasA) d_unpack(A.d, al, ah);
+                int dec = nh < __dmul_rn(bt.weight, al) ? 1 : (nl >= __dmul_rn(bt.weight, ah) ? 0 : -1);
+                if (dec < 0) {
+                    double* xs = reinterpret_cast<double*>(smem + L.apk + 32);
+                    if (warp == 0) {
+                        const double d = exact_pair(N.lo, N.hi);
+                        if (lane == 0) xs[0] = d;
+                    } else if (warp == 1 && hasA) {
+                        const double d = exact_pair(A.lo, A.hi);
+                        if (lane == 0) xs[1] = d;
+                    }
+                    __syncthreads();
+                    N.d = xs[0];
+                    if (hasA) A.d = xs[1];
+                    dec = N.d < __dmul_rn(bt.weight, hasA ? A.d : kInf) ? 1 : 0;
+                }
+                if (dec) { a = N.lo; b = N.hi; dch = N.d; kind = 1; }
+            } else {
+                const double da = hasA ? A.d : kInf;
+                if (N.d < __dmul_rn(bt.weight, da)) { a = N.lo; b = N.hi; dch = N.d; kind = 1; }
+            }
         }
         if (a < 0 && hasA) { a = A.lo; b = A.hi; dch = A.d; kind = 0; }
         if (a < 0) {
             conv = 1;
-            if (SPEC) {  // drain the copies put in flight for this step
+            if (STREAM) {  // drain the copies put in flight for this step
                 for (int i = 0; i < min(NS, ss.nst); ++i) {
                     const uint32_t g = ss.base + i;
                     mbar_wait(&bars[g % NS], (g / NS) & 1u);
@@ -1114,28 +1257,29 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 if (RHSEG_RESCAN_PREFETCH) bulk_prefetch_l2(D + (size_t)i * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
             }
         }
+        if (APO && tid == 0) {  // rows a and b feed the row-a' pass after the merge
+            bulk_prefetch_l2(D + (size_t)a * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
+            bulk_prefetch_l2(D + (size_t)b * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
+        }
         // (C) merge (graph.py:229-264) on this CTA's private copies
         const double nn = __dadd_rn((double)cnt[a], (double)cnt[b]);
         const bool own_a = a >= lo && a < hi;
+        const double na0 = (double)cnt[a], nb0 = (double)cnt[b];  // (APO: the log's exact value, in C2)
+        ApoStep ap{};
+        if (APO) ap = apo_step<M>(na0, nb0, dch, apoE, apoEe);
         {
             double* sa = sums + (size_t)a * B;
             const double* sb = sums + (size_t)b * B;
-            SE* mu_a = SPEC ? (own_a ? (ss.cur ? sb1 : sb0) + lo + slot_of[a - lo] : nullptr)
-                            : reinterpret_cast<SE*>(mu0 + a);
+            SE* mu_a = STREAM ? (own_a ? (ss.cur ? sb1 : sb0) + lo + slot_of[a - lo] : nullptr)
+                              : (SPEC ? nullptr : mu0 + a);
             for (int k = tid; k < B; k += kThreads) {
                 const double s = __dadd_rn(sa[k], sb[k]);
                 sa[k] = s;
                 const double m = __ddiv_rn(s, nn);
-                mua[k] = m;
-                if (F32) {
-                    const float x = __double2float_rn(__dsub_rn(m, (double)fref[k]));
-                    fxa[k] = x;
-                    if (own_a) mu_a[(size_t)k * Rp] = (SE)x;
-                } else if (own_a) {
-                    mu_a[(size_t)k * Rp] = (SE)m;
-                }
+                mua[k] = m;  // (APO: written to mr row R0 + step at the end of the step)
+                if ((STREAM || !SPEC) && own_a) mu_a[(size_t)k * Rp] = m;
             }
-            if (SPEC && own_a) fence_proxy_async_global();
+            if (STREAM && own_a) fence_proxy_async_global();
         }
         uint32_t* ra = adj + (size_t)a * W;
         {
@@ -1189,6 +1333,8 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 bt.log_a[o] = a;
                 bt.log_b[o] = b;
                 bt.log_d[o] = dch;
+                if (APO && d_is_interval(dch))  // exact value after the loop (versions of a and b)
+                    bt.apo_rec[o] = make_uint4(ver[a], ver[b], (unsigned)na0, (unsigned)nb0);
                 bt.log_k[o] = (uint8_t)kind;
                 bt.parent[(size_t)sec * Rp + b] = a;
                 if (SPEC) {
@@ -1262,7 +1408,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     }
                     __syncthreads();
                 }
-            } else if (F32) {
+            } else if (APO) {
                 for (int k = warp; k < ni; k += kWarps) rescanf(inv[k] >> 2, inv[k] & 3, a);
             } else {
                 for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
@@ -1272,22 +1418,10 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
-        double n2a = 0.0, xna = 0.0;
-        if (F32) {  // ||x_a|| upper bound (any summation order: it only widens intervals)
-            double* sx = reinterpret_cast<double*>(misc + 8);
-            if (warp == 0) {
-                double v = 0.0;
-                for (int k = lane; k < B; k += 32) v += (double)fxa[k] * (double)fxa[k];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) {
-                    *sx = sqrt(v) * (1.0 + 1e-6) + 1e-300;
-                    if (own_a) bt.xnorm[(size_t)sec * Rp + a] = *sx;
-                }
-            }
+        double n2a = 0.0;
+        if (APO) {
             if (tid == 0) sScan = 0;
             __syncthreads();
-            xna = *sx;
         }
         if (M == kSam) {  // squared norm of a's new mean, sequential (oracle order)
             double* sn2a = reinterpret_cast<double*>(misc + 6);
@@ -1314,76 +1448,82 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                 isadj[q] = valid[q] && ((sra[j >> 5] >> (j & 31)) & 1u);
                 s[q] = 0.0;
             }
-            for (int i = 0; i < ss.nst; ++i) {
-                const uint32_t g = ss.base + i;
-                mbar_wait(&bars[g % NS], (g / NS) & 1u);
-                const SE* tile = reinterpret_cast<const SE*>(ring) + (size_t)(g % NS) * (SB / ES);
-                const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
-                // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
-                // accumulate garbage that the epilogue discards via valid[])
-                switch (nq) {
+            if (STREAM) {
+                for (int i = 0; i < ss.nst; ++i) {
+                    const uint32_t g = ss.base + i;
+                    mbar_wait(&bars[g % NS], (g / NS) & 1u);
+                    const SE* tile = reinterpret_cast<const SE*>(ring) + (size_t)(g % NS) * (SB / ES);
+                    const int k0 = i * ss.KB, kb = min(ss.KB, B - k0);
+                    // exactly nq columns per thread, unpredicated (slots >= S, holes, a and b
+                    // accumulate garbage that the epilogue discards via valid[])
+                    switch (nq) {
 #define RHSEG_CONSUME(NQC)                                                        \
     case NQC:                                                                     \
         for (int kk = 0; kk < kb; ++kk) {                                         \
-            const double m = F32 ? (double)fxa[k0 + kk] : mua[k0 + kk];           \
+            const double m = mua[k0 + kk];                                        \
             const SE* row = tile + (size_t)kk * ss.S2 + tid;                      \
             _Pragma("unroll") for (int q = 0; q < NQC; ++q) s[q] = acc_step<M>(s[q], m, (double)row[q * kThreads]); \
         }                                                                         \
         break;
-                    RHSEG_CONSUME(1) RHSEG_CONSUME(2) RHSEG_CONSUME(3) RHSEG_CONSUME(4)
-                    RHSEG_CONSUME(5) RHSEG_CONSUME(6) RHSEG_CONSUME(7) RHSEG_CONSUME(8)
+                        RHSEG_CONSUME(1) RHSEG_CONSUME(2) RHSEG_CONSUME(3) RHSEG_CONSUME(4)
+                        RHSEG_CONSUME(5) RHSEG_CONSUME(6) RHSEG_CONSUME(7) RHSEG_CONSUME(8)
 #undef RHSEG_CONSUME
-                    default: break;
-                }
-                __syncthreads();  // slot g % NS is free again
-                if (i + NS < ss.nst) {
-                    if (warp == 0) issue_stage(g + NS, i + NS);
-                }
-            }
-            ss.issued += max(0, ss.nst - NS);
-            if (F32) {
-                // an interval around every d(a, j) goes to D; offers compare
-                // intervals and only an overlap with row j's cached best is resolved
-                // exactly. a's own best: the columns whose lower bound reaches below
-                // the stage's smallest upper bound -- one is kept as an interval,
-                // several are made exact.
-                const double* xn = bt.xnorm + (size_t)sec * Rp;
-                double dlo[NQ], dhi[NQ];
-                double uA = kInf, uN = kInf;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    dlo[q] = kInf;
-                    dhi[q] = kInf;
-                    if (valid[q]) {
-                        f32_interval<M>(s[q], xna + xn[jq[q]], nn, (double)cnt[jq[q]], B, dlo[q], dhi[q]);
-                        if (isadj[q]) uA = fmin(uA, dhi[q]);
-                        else uN = fmin(uN, dhi[q]);
+                        default: break;
+                    }
+                    __syncthreads();  // slot g % NS is free again
+                    if (i + NS < ss.nst) {
+                        if (warp == 0) issue_stage(g + NS, i + NS);
                     }
                 }
-                int* cntF = misc + 10;  // [0] overlaps, [1] a-candidates adjacent, [2] non-adjacent
-                if (tid == 0) { cntF[0] = 0; cntF[1] = 0; cntF[2] = 0; }
-                {
-                    RowBest x{uA, 0}, y{uN, 0};
-                    block_min_rb2(x, y, rscr);
-                    uA = x.d;
-                    uN = y.d;
-                }
-                unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);  // overlaps
-                unsigned short* l2 = l1 + Rs;                                 // a's candidates
-                // (l1 and l2 each hold at most one entry per own column)
+                ss.issued += max(0, ss.nst - NS);
+            }
+            if (APO) {
+                // an interval around every d(a', j) (from D rows a and b) goes to D;
+                // an offer is resolved exactly only when its lower bound reaches row j's
+                // (exact) cached best. a's own best: the exact lexicographic minimum of
+                // the columns whose lower bound reaches the stage's smallest upper bound.
+                const double* Da = D + (size_t)a * Rp;
+                const double* Db = D + (size_t)b * Rp;
+                double* sdl = reinterpret_cast<double*>(smem + L.sdv);  // per own slot: d(a, j) -> lower bound
+                double* sdh = sdl + Rs;                                 //               d(b, j) -> upper bound
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    if (!valid[q]) continue;
-                    const int j = jq[q], r = j - lo;
-                    const bool aj = isadj[q];
+                for (int q = 0; q < NQ; ++q) {  // all loads in flight first
+                    if (valid[q]) {
+                        const int sl = tid + q * kThreads;
+                        sdl[sl] = __ldcg(Da + jq[q]);
+                        sdh[sl] = __ldcg(Db + jq[q]);
+                    }
+                }
+                int* cntF = misc + 10;  // offers that need the exact d(a', j)
+                if (tid == 0) { cntF[0] = 0; ak[6] = 0u; ak[7] = 0u; }
+                __syncthreads();
+                unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);  // exact offers
+                unsigned short* l2 = l1 + Rs;                                 // a's candidates
+                // (l1 and l2 each hold at most one entry per own column; entry = j |
+                // 0x4000 non-adjacent stage | 0x8000 interval too wide to store)
+                double uA = kInf, uN = kInf;
+#pragma unroll 1
+                for (int sl = tid; sl < ss.S; sl += kThreads) {
+                    const int j = col[sl];
+                    if (j < 0 || j == a || j == b || cnt[j] == 0u) continue;
+                    const bool aj = (sra[j >> 5] >> (j & 31)) & 1u;
+                    const int r = j - lo;
+                    double dlo, dhi;
+                    apo_interval<M>(ap, sdl[sl], sdh[sl], (double)cnt[j], dlo, dhi);
+                    sdl[sl] = dlo;
+                    sdh[sl] = dhi;
+                    if (aj) uA = fmin(uA, dhi);
+                    else uN = fmin(uN, dhi);
                     const unsigned short e = (unsigned short)(j | (aj ? 0 : 0x4000));
-                    const double v = d_pack_interval(dlo[q], dhi[q]);
+                    double v;
+                    if (!d_pack_interval(dlo, dhi, v)) {  // exact d(a', j) below, then the offer
+                        l1[atomicAdd(&cntF[0], 1)] = (unsigned short)(e | 0x8000);
+                        continue;
+                    }
                     D[(size_t)j * Rp + a] = v;
                     D[(size_t)a * Rp + j] = v;
-                    if (dlo[q] <= (aj ? uA : uN)) {
-                        l2[atomicAdd(&sScan, 1)] = e;
-                        atomicAdd(&cntF[aj ? 1 : 2], 1);
-                    }
+                    // offer (d(a', j), a) to row j: decided on the intervals unless they
+                    // overlap (then both sides are made exact below)
                     double& bv = aj ? bAd[r] : bNd[r];
                     int& bj = aj ? bAj[r] : bNj[r];
                     if (bj < 0) {
@@ -1392,48 +1532,64 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
                     } else {
                         double bl, bh;
                         d_unpack(bv, bl, bh);
-                        if (dhi[q] < bl) { bv = v; bj = a; }
-                        else if (!(dlo[q] > bh)) l1[atomicAdd(&cntF[0], 1)] = e;
+                        if (dhi < bl) { bv = v; bj = a; }
+                        else if (!(dlo > bh)) l1[atomicAdd(&cntF[0], 1)] = e;
+                    }
+                }
+                {
+                    RowBest x{uA, 0}, y{uN, 0};
+                    block_min_rb2(x, y, rscr);
+                    uA = x.d;
+                    uN = y.d;
+                }
+#pragma unroll 1
+                for (int sl = tid; sl < ss.S; sl += kThreads) {
+                    const int j = col[sl];
+                    if (j < 0 || j == a || j == b || cnt[j] == 0u) continue;
+                    const bool aj = (sra[j >> 5] >> (j & 31)) & 1u;
+                    if (sdl[sl] <= (aj ? uA : uN)) {
+                        l2[atomicAdd(&sScan, 1)] = (unsigned short)(j | (aj ? 0 : 0x4000));
+                        atomicAdd(&ak[aj ? 6 : 7], 1u);
                     }
                 }
                 __syncthreads();
-                const int n1 = cntF[0], n2 = sScan, nA = cntF[1], nN = cntF[2];
-                // overlaps with row j's cached best: exact d(a, j) and exact best
+                const int n1 = cntF[0], n2 = sScan;
+                if (bt.prof && tid == 0) {
+                    atomicAdd(bt.prof + 8, (unsigned long long)n1);
+                    atomicAdd(bt.prof + 9, (unsigned long long)n2);
+                }
+                // overlaps with row j's cached best: exact d(a', j) and exact best
                 for (int t = warp; t < n1; t += kWarps) {
                     const int e = l1[t], j = e & 0x3fff, r = j - lo;
-                    const bool aj = !(e >> 14);
-                    const double* sj = sums + (size_t)j * B;
-                    const double cj = (double)cnt[j];
-                    const double daj = warp_exact<M>(mua, nullptr, nn, sj, cj, B, lane);
+                    const bool aj = !(e & 0x4000);
+                    const double daj = warp_exact<M>(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane);
                     const int bj = aj ? bAj[r] : bNj[r];
                     double db = aj ? bAd[r] : bNd[r];
-                    const bool binterval = d_is_interval(db);
-                    if (binterval) db = warp_exact<M>(nullptr, sj, cj, sums + (size_t)bj * B, (double)cnt[bj], B, lane);
+                    const bool binterval = bj >= 0 && d_is_interval(db);
+                    if (binterval) db = exact_pair(j, bj);
                     if (lane == 0) {
                         D[(size_t)j * Rp + a] = daj;
                         D[(size_t)a * Rp + j] = daj;
-                        if (binterval) {
-                            D[(size_t)j * Rp + bj] = db;
-                            D[(size_t)bj * Rp + j] = db;
-                        }
-                        const bool take_a = daj < db || (daj == db && a < bj);
+                        const bool take_a = bj < 0 || daj < db || (daj == db && a < bj);
                         if (aj) { bAd[r] = take_a ? daj : db; bAj[r] = take_a ? a : bj; }
                         else { bNd[r] = take_a ? daj : db; bNj[r] = take_a ? a : bj; }
                     }
                 }
                 __syncthreads();
-                // a's best per stage
+                // a's best per stage: a single candidate is the minimum as it is
+                // (interval or not); several are compared exactly
+                const int nA = ak[6], nN = ak[7];
                 for (int t = warp; t < n2; t += kWarps) {
                     const int e = l2[t], j = e & 0x3fff;
-                    const bool aj = !(e >> 14);
-                    if ((aj ? nA : nN) == 1) {
+                    const bool aj = !(e & 0x4000);
+                    const double v = __ldcg(D + (size_t)a * Rp + j);
+                    if ((aj ? nA : nN) == 1 || !d_is_interval(v)) {
                         if (lane == 0) {
-                            const RowBest c{D[(size_t)a * Rp + j], j};
-                            if (aj) pA = c;
-                            else pN = c;
+                            if (aj) rb_offer_iv(pA, v, j);
+                            else rb_offer_iv(pN, v, j);
                         }
                     } else {
-                        const double d = warp_exact<M>(mua, nullptr, nn, sums + (size_t)j * B, (double)cnt[j], B, lane);
+                        const double d = warp_exact<M>(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane);
                         if (lane == 0) {
                             D[(size_t)j * Rp + a] = d;
                             D[(size_t)a * Rp + j] = d;
@@ -1483,6 +1639,10 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             }
         }
         if (SPEC) block_min_rb2(pA, pN, rscr);
+        if (APO) {  // a's new mean becomes version R0 + step (the old one stays for the log)
+            for (int k = tid; k < B; k += kThreads) mr[(size_t)(R0 + step) * B + k] = mua[k];
+            if (tid == 0) ver[a] = (unsigned short)(R0 + step);
+        }
         else pA = block_min_rb(pA, rscr);
         if (tid == 0) {
             rpart[0] = pA;
@@ -1501,6 +1661,21 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         mark(3);
         a_prev = a;
         ++step;
+    }
+    if (APO) {
+        // the log's dissimilarities still held as intervals: exact values now, one
+        // thread per step (the reference's ascending-band sum from the two versions)
+        __syncthreads();
+        for (int t = tid; t < step; t += kThreads) {
+            const size_t o = (size_t)sec * Rp + t;
+            if (!d_is_interval(bt.log_d[o])) continue;
+            const uint4 rc = bt.apo_rec[o];
+            const double* mi = mr + (size_t)rc.x * B;
+            const double* mj = mr + (size_t)rc.y * B;
+            double sacc = 0.0;
+            for (int k = 0; k < B; ++k) sacc = acc_step<M>(sacc, mi[k], mj[k]);
+            bt.log_d[o] = pair_finish<M>((double)rc.z, (double)rc.w, sacc, 0.0, 0.0);
+        }
     }
     if (CLUSTER) cluster_barrier();  // keep our slots alive until every peer is done reading
     if (bt.prof && tid == 0) {
@@ -1528,9 +1703,12 @@ int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
         RHSEG_PICK(kSam)
     } else if (b.measure == kEuclid) {
         RHSEG_PICK(kEuclid)
+        if (b.apo) kern = hseg_loop_kernel<false, true, kEuclid, true>;
     } else {
         RHSEG_PICK(kBsmse)
+        if (b.apo) kern = hseg_loop_kernel<false, true, kBsmse, true>;
     }
+    if (b.apo && !apo_capable(b.spec != 0, b.C, b.measure)) return cudaErrorInvalidValue;
 #undef RHSEG_PICK
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

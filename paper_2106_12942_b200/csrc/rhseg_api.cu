@@ -240,8 +240,13 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     // rings for levels with at most one CTA per SM were both measured slower on C2
     // (47 -> 87 / 82 ms): the shared-memory carveout takes the L1 that the
     // adjacency and sums accesses live in.
+    // APO (default where capable; RHSEG_APO=0 selects the mean-stream loop): row a' is
+    // bounded from D rows a and b: no stream ring; the second mean buffer holds the
+    // region-major means the exact re-evaluations read
+    const char* apo_env = getenv("RHSEG_APO");
+    const bool apo = hseg_apo_capable(spec, lv.C, lv.measure) && !(apo_env && apo_env[0] == '0');
     const int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
-    const int nstages = hseg_loop_default_stages();
+    const int nstages = apo ? 0 : hseg_loop_default_stages();
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
@@ -264,10 +269,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     o = 0;
     const size_t oAdj = take(ns * C * Rp * W * 4);
     lv.work_zero = o;
-    const bool f32 = hseg_use_f32(spec, lv.C, lv.measure);
-    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec && !f32 ? ns * B * Rp * 8 : 0),
-                 oM32 = take(f32 ? ns * B * Rp * 4 : 0), oM32b = take(f32 ? ns * B * Rp * 4 : 0),
-                 oXn = take(f32 ? ns * Rp * 8 : 0),
+    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec ? (apo ? 2 : 1) * ns * B * Rp * 8 : 0),  // APO: versioned means
+                 oRec = take(apo ? ns * Rp * 16 : 0),
                  oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
     {
@@ -289,6 +292,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.spec = spec ? 1 : 0;
     b.stage_bytes = stage_bytes;
     b.nstages = nstages;
+    b.apo = apo ? 1 : 0;
     // a level whose streamed means fit the persisting L2 set-aside keeps them there
     b.l2_window_base = nullptr;
     b.l2_window_bytes = 0;
@@ -316,10 +320,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.pairs = reinterpret_cast<long long*>(K + oPr);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
-    b.mu2 = spec && !f32 ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
-    b.mu32 = f32 ? reinterpret_cast<float*>(Wk + oM32) : nullptr;
-    b.mu32b = f32 ? reinterpret_cast<float*>(Wk + oM32b) : nullptr;
-    b.xnorm = f32 ? reinterpret_cast<double*>(Wk + oXn) : nullptr;
+    b.mu2 = spec ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.apo_rec = apo ? reinterpret_cast<uint4*>(Wk + oRec) : nullptr;
     b.sums = reinterpret_cast<double*>(Wk + oSums);
     lv.map = reinterpret_cast<int*>(K + oMap);
     CK(cudaMemcpyAsync(const_cast<int*>(b.R0), lv.R0h.data(), ns * 4, cudaMemcpyHostToDevice, st));
@@ -363,8 +365,8 @@ struct LeafPipe {
 static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* pipe = nullptr) {
     unsigned long long* prof = nullptr;
     if (profiling()) {
-        CK(cudaMallocAsync(&prof, 8 * 8, st));
-        CK(cudaMemsetAsync(prof, 0, 8 * 8, st));
+        CK(cudaMallocAsync(&prof, 16 * 8, st));
+        CK(cudaMemsetAsync(prof, 0, 16 * 8, st));
     }
     lv.sb.prof = prof;
     const double t_enter = prof ? now_ms() : 0.0;
@@ -449,8 +451,8 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
     CK(cudaMemcpyAsync(lv.nlogh.data(), lv.sb.nlog, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.convh.data(), lv.sb.conv, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.pairsh.data(), lv.sb.pairs, 8 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
-    unsigned long long ph[8] = {0};
-    if (prof) CK(cudaMemcpyAsync(ph, prof, 8 * 8, cudaMemcpyDeviceToHost, st));
+    unsigned long long ph[16] = {0};
+    if (prof) CK(cudaMemcpyAsync(ph, prof, 16 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (lv.sb.l2_window_bytes) cudaCtxResetPersistingL2Cache();  // hand the set-aside back
     RHSEG_TRACE("run_level %d: synced", lv.level);
@@ -464,6 +466,11 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
                 lv.level, lv.nsec, lv.C, lv.Rp, steps, tot / (double)std::max(1LL, steps) / lv.C,
                 100 * ph[0] / tot, 100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot,
                 (double)ph[5] / (double)std::max(1LL, steps));
+        if (ph[8] + ph[9] + ph[11])
+            fprintf(stderr, "[rhseg profile] level %d APO per step: %.2f exact offers, %.2f a-candidates, "
+                    "%.2f rescan exact pairs (%.0f cycles each)\n", lv.level, (double)ph[8] / std::max(1LL, steps),
+                    (double)ph[9] / std::max(1LL, steps), (double)ph[11] / std::max(1LL, steps),
+                    (double)ph[12] / std::max(1ULL, ph[11]));
         cudaFree(prof);
         fprintf(stderr, "[rhseg profile] level %d host wall in run_level %.2f ms; per CTA: prologue %.0f cycles, "
                 "kernel %.0f cycles\n", lv.level, now_ms() - t_enter, (double)ph[6] / (lv.nsec * lv.C),

@@ -19,6 +19,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <vector_types.h>
+
 namespace rhseg {
 
 struct SectionBatch {
@@ -33,6 +35,7 @@ struct SectionBatch {
     int measure;   // 0 sqrt-bsmse (reference), 1 euclidean, 2 sam (extensions)
     int stage_bytes;  // merge-loop stream ring stage size (host-chosen)
     int nstages;      // merge-loop stream ring depth (host-chosen)
+    int apo;          // merge loop bounds d(a', j) from D rows a, b (no mean stream; see hseg_kernels.cu)
     void* l2_window_base;    // L2-persisting access window of the loop launch (0 bytes = none)
     size_t l2_window_bytes;
     double weight; // spectral_weight (engine.py:33)
@@ -40,9 +43,7 @@ struct SectionBatch {
     const int* target;   // [nsec] stopping count (recursive.py:49-52)
     double* mu;
     double* nrm2;        // [nsec][Rp] squared norm of each mean vector (sam only, else nullptr)
-    float* mu32;         // F32 filter: [nsec][B][Rp] centred fp32 means (compacted stream), ping-pong
-    float* mu32b;        //   second buffer of the ping-pong
-    double* xnorm;       //   [nsec][Rp] upper bound of ||centred fp32 mean||_2 per region
+    uint4* apo_rec;      // APO: [nsec][Rp] (mean versions of a, b; counts) of steps logged as intervals
     double* mu2;         // second mean buffer: the loop kernel compacts live columns into it (w > 0)
     double* D;
     double* sums;
@@ -74,7 +75,7 @@ int hseg_loop_max_stages();
 int hseg_loop_default_stages();
 int hseg_loop_stage_bytes(bool spec, int C, int measure);  // default ring stage size
 int hseg_loop_max_rows();  // own rows per CTA the loop kernel supports
-bool hseg_use_f32(bool spec, int C, int measure);  // the loop streams fp32 filter means
+bool hseg_apo_capable(bool spec, int C, int measure);  // the loop can run without the mean stream
 // sections [b.sec0, b.sec0 + count) of the leaf level (count < 0: through the end)
 void launch_leaf_init(const SectionBatch& b, const float* cube, int img_edge, int cols, int row0,
                       int col0, int connectivity, cudaStream_t st, int count = -1);
