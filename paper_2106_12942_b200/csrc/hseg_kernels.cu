@@ -208,7 +208,7 @@ constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per merge
 
 struct LoopSmem {
-    size_t ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -245,6 +245,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.sdv = o;   o = align16(o + (spec && nstages == 0 ? Rs * 16 : 0));  // APO: per-slot D values / bounds
     L.apk = o;   o += 64;                                                  // APO: argmin keys, rule scratch
     L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
+    L.livew = o; o = align16(o + (spec && nstages == 0 ? (size_t)(Rp / 32) * 4 : 0));  // APO: live-region bitset
     o = (o + 127) & ~size_t(127);
     L.ring = o;
     o += spec && nstages > 0 ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;  // (APO: no ring)
@@ -532,8 +533,11 @@ struct StreamState {
 #ifndef RHSEG_MINBLOCKS
 #define RHSEG_MINBLOCKS 2
 #endif
+#ifndef RHSEG_APO_MINBLOCKS
+#define RHSEG_APO_MINBLOCKS 2
+#endif
 template <bool CLUSTER, bool SPEC, int M, bool APO = false>
-__global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
+__global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
     const long long t_entry = clock64();
     const int C = CLUSTER ? bt.C : 1;
@@ -597,6 +601,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
     // the log's exact values are computed after the loop from (old a, b) versions
     double* const mr = APO ? bt.mu2 + 2 * sec * bt.mu_stride() : nullptr;
     unsigned short* ver = reinterpret_cast<unsigned short*>(smem + L.ver);  // APO: region -> mr row
+    uint32_t* livew = reinterpret_cast<uint32_t*>(smem + L.livew);          // APO: live regions
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
@@ -713,29 +718,34 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         }
         return d;
     };
-    auto rescanf = [&](int i, int mask, int ex) {
+    auto rescanf_full = [&](int i, int mask, int ex) {
         const uint32_t* arow = adj + (size_t)i * W;
         double* drow = D + (size_t)i * Rp;
         const bool live_i = cnt[i] != 0u;
         Lo2 xa{kInf, kInf, kInf, kInf, kNoJ}, xn{kInf, kInf, kInf, kInf, kNoJ};
-        constexpr int U = 16;
+        constexpr int U = 8;
         if (live_i) {
-            for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+            // id-ordered walk, one bitset word per warp-iteration: lane l takes id
+            // 32 w + l, whose liveness and adjacency bits come from two broadcast words,
+            // and the D loads of a warp are one contiguous 256-byte row segment
+            for (int w0 = 0; w0 < W; w0 += U) {
                 double dv[U];
-                int jv[U];
+                uint32_t sel[U];  // bit0: candidate, bit1: adjacent
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int sl = s0 + 32 * u + lane;
-                    const int j = sl < ss.S ? col[sl] : -1;
-                    jv[u] = j;
-                    dv[u] = j >= 0 ? __ldcs(drow + j) : kInf;
+                    const int w = w0 + u;
+                    const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
+                    const int j = (w << 5) + lane;
+                    const bool aj = (aw >> lane) & 1u;
+                    const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (mask & 1) : (mask & 2));
+                    sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                    dv[u] = c ? __ldcs(drow + j) : kInf;
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int j = jv[u];
-                    if (j < 0 || j == i || j == ex || cnt[j] == 0u) continue;
-                    const bool aj = (arow[j >> 5] >> (j & 31)) & 1u;
-                    if (aj ? !(mask & 1) : !(mask & 2)) continue;
+                    if (!(sel[u] & 1u)) continue;
+                    const int j = ((w0 + u) << 5) + lane;
+                    const bool aj = sel[u] & 2u;
                     double lo2, hi2;
                     d_unpack(dv[u], lo2, hi2);
                     Lo2& x = aj ? xa : xn;
@@ -801,6 +811,84 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (mask & 1) { bAd[r] = ba.d; bAj[r] = ba.j == kNoJ ? -1 : ba.j; }
             if (mask & 2) { bNd[r] = bn.d; bNj[r] = bn.j == kNoJ ? -1 : bn.j; }
         }
+    };
+
+    // APO rescan, fast path: one pass over the row keeps, per stage, the smallest and
+    // second smallest approximate value (the raw D bits with the sign cleared: the
+    // exact value, or an interval's centre to 2^-46) and the widest interval code seen.
+    // If the smallest entry's upper bound lies below every other entry's lower bound
+    // (bounded via the second smallest centre and the widest code), it is the row's
+    // minimum; otherwise that stage falls back to rescanf_full.
+    struct C2x {
+        double c1, v1, c2;
+        int j1, kmax;
+    };
+    auto c2_put = [](C2x& x, double c, int j, double v) {
+        if (c < x.c1 || (c == x.c1 && j < x.j1)) {
+            x.c2 = x.c1;
+            x.c1 = c; x.j1 = j; x.v1 = v;
+        } else if (c < x.c2) {
+            x.c2 = c;
+        }
+    };
+    auto c2_unique = [](const C2x& x) {
+        if (x.c2 == kInf) return true;
+        double l1, h1;
+        d_unpack(x.v1, l1, h1);
+        const double rho = __longlong_as_double((long long)(x.kmax - 46 + 1023) << 52) + 0x1p-45;
+        return h1 < __dmul_rd(x.c2, __dsub_rd(1.0, rho));
+    };
+    auto rescanf = [&](int i, int mask, int ex) {
+        const uint32_t* arow = adj + (size_t)i * W;
+        const double* drow = D + (size_t)i * Rp;
+        C2x xa{kInf, kInf, kInf, kNoJ, 0}, xn{kInf, kInf, kInf, kNoJ, 0};
+        constexpr int U = 8;
+        if (cnt[i] != 0u) {
+            for (int w0 = 0; w0 < W; w0 += U) {
+                double dv[U];
+                uint32_t sel[U];  // bit0: candidate, bit1: adjacent
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int w = w0 + u;
+                    const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
+                    const int j = (w << 5) + lane;
+                    const bool aj = (aw >> lane) & 1u;
+                    const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (mask & 1) : (mask & 2));
+                    sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                    dv[u] = c ? __ldcs(drow + j) : kInf;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (!(sel[u] & 1u)) continue;
+                    const long long r = __double_as_longlong(dv[u]);
+                    C2x& x = (sel[u] & 2u) ? xa : xn;
+                    x.kmax = max(x.kmax, r < 0 ? (int)(r & 63) : 0);
+                    c2_put(x, __longlong_as_double(r & 0x7fffffffffffffffLL), ((w0 + u) << 5) + lane, dv[u]);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int st = 0; st < 2; ++st) {
+                C2x& x = st ? xn : xa;
+                const double c1 = __shfl_xor_sync(0xffffffffu, x.c1, o), v1 = __shfl_xor_sync(0xffffffffu, x.v1, o);
+                const double c2 = __shfl_xor_sync(0xffffffffu, x.c2, o);
+                const int j1 = __shfl_xor_sync(0xffffffffu, x.j1, o), km = __shfl_xor_sync(0xffffffffu, x.kmax, o);
+                x.kmax = max(x.kmax, km);
+                if (j1 != kNoJ) c2_put(x, c1, j1, v1);
+                if (c2 < x.c2) x.c2 = c2;
+            }
+        }
+        int slow = 0;
+        if ((mask & 1) && xa.j1 != kNoJ && !c2_unique(xa)) slow |= 1;
+        if ((mask & 2) && xn.j1 != kNoJ && !c2_unique(xn)) slow |= 2;
+        if (lane == 0) {
+            const int r = i - lo;
+            if ((mask & 1) && !(slow & 1)) { bAd[r] = xa.v1; bAj[r] = xa.j1 == kNoJ ? -1 : xa.j1; }
+            if ((mask & 2) && !(slow & 2)) { bNd[r] = xn.v1; bNj[r] = xn.j1 == kNoJ ? -1 : xn.j1; }
+        }
+        if (slow) rescanf_full(i, slow, ex);
     };
 
     // TOP2 rescan: the two best candidates per masked stage + the complete bit,
@@ -989,6 +1077,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
             if (cnt[i] != 0u) mr[e] = __ddiv_rn(sums[e], (double)cnt[i]);  // == the cached mean, bit for bit
         }
         for (int i = tid; i < Rp; i += kThreads) ver[i] = (unsigned short)i;
+        for (int w = tid; w < W; w += kThreads) {
+            uint32_t m = 0u;
+            for (int t = 0; t < 32; ++t) m |= (cnt[(w << 5) + t] != 0u ? 1u : 0u) << t;
+            livew[w] = m;
+        }
+        __syncthreads();
         apoEe = sqrt(*sx * (1.0 + 1e-9)) * (10.0 * kU64 * 1.01);  // see apo_interval
         __syncthreads();
     }
@@ -1324,6 +1418,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_MINBLOCKS) hseg_loop_kernel(Se
         if (tid == 0) {
             cnt[a] = (uint32_t)nn;
             cnt[b] = 0u;
+            if (APO) livew[b >> 5] &= ~(1u << (b & 31));
             if (own_a) {
                 bAd[a - lo] = kInf; bAj[a - lo] = -1;
                 bNd[a - lo] = kInf; bNj[a - lo] = -1;
