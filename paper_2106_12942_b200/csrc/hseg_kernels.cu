@@ -813,40 +813,70 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         }
     };
 
-    // APO rescan, fast path: one pass over the row keeps, per stage, the smallest and
-    // second smallest approximate value (the raw D bits with the sign cleared: the
-    // exact value, or an interval's centre to 2^-46) and the widest interval code seen.
-    // If the smallest entry's upper bound lies below every other entry's lower bound
-    // (bounded via the second smallest centre and the widest code), it is the row's
-    // minimum; otherwise that stage falls back to rescanf_full.
-    struct C2x {
-        double c1, v1, c2;
-        int j1, kmax;
-    };
-    auto c2_put = [](C2x& x, double c, int j, double v) {
-        if (c < x.c1 || (c == x.c1 && j < x.j1)) {
-            x.c2 = x.c1;
-            x.c1 = c; x.j1 = j; x.v1 = v;
-        } else if (c < x.c2) {
-            x.c2 = c;
-        }
-    };
-    auto c2_unique = [](const C2x& x) {
-        if (x.c2 == kInf) return true;
+    // APO rescan, fast path: one branch-free pass over the row keeps, per stage, the
+    // two smallest 64-bit keys (D bits with the sign cleared -- the exact value or an
+    // interval's centre -- truncated by 14 bits, with the column id in the low 14 bits:
+    // non-negative doubles order like their bit patterns) and the widest interval code.
+    // If the smallest key's entry has its upper bound below the lower bound of every
+    // other entry (bounded through the second key and the widest code), it is the
+    // row's minimum; otherwise that stage falls back to rescanf_full.
+    constexpr unsigned long long kKeyHi = 0x7fffffffffffc000ULL, kKeyNone = ~0ULL;
+    auto key_unique = [&](unsigned long long k1, unsigned long long k2, int kmax, const double* drow,
+                          double& v1) {
+        v1 = __ldcg(drow + (int)(k1 & 0x3fff));
+        if (k2 == kKeyNone) return true;
         double l1, h1;
-        d_unpack(x.v1, l1, h1);
-        const double rho = __longlong_as_double((long long)(x.kmax - 46 + 1023) << 52) + 0x1p-45;
-        return h1 < __dmul_rd(x.c2, __dsub_rd(1.0, rho));
+        d_unpack(v1, l1, h1);
+        // other entries: centre >= c2 (truncated: relative 2^-38), interval >= centre (1 - rho)
+        const double c2 = __longlong_as_double((long long)(k2 & kKeyHi));
+        const double rho = __longlong_as_double((long long)(kmax - 46 + 1023) << 52) + 0x1p-37;
+        return h1 < __dmul_rd(c2, __dsub_rd(1.0, rho));
     };
     auto rescanf = [&](int i, int mask, int ex) {
         const uint32_t* arow = adj + (size_t)i * W;
         const double* drow = D + (size_t)i * Rp;
-        C2x xa{kInf, kInf, kInf, kNoJ, 0}, xn{kInf, kInf, kInf, kNoJ, 0};
+        unsigned long long a1 = kKeyNone, a2 = kKeyNone, n1 = kKeyNone, n2 = kKeyNone;
+        int km = 0;  // widest interval code over both stages (only widens the test)
         constexpr int U = 8;
-        if (cnt[i] != 0u) {
+        auto take = [&](double v, int j, bool c, bool aj) {
+            const unsigned long long r = (unsigned long long)__double_as_longlong(v);
+            km = max(km, (int)(r >> 63) * (int)(r & 63));
+            const unsigned long long key = c ? ((r & kKeyHi) | (unsigned long long)j) : kKeyNone;
+            const unsigned long long ka = aj ? key : kKeyNone, kn = aj ? kKeyNone : key;
+            a2 = min(a2, max(a1, ka));
+            a1 = min(a1, ka);
+            n2 = min(n2, max(n1, kn));
+            n1 = min(n1, kn);
+        };
+        if (cnt[i] != 0u && 2 * ss.S < R0) {
+            // sparse (most regions merged away): walk the compacted live-column list
+            for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                double dv[U];
+                int jv[U];
+                uint32_t sel[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int sl = s0 + 32 * u + lane;
+                    const int j = sl < ss.S ? col[sl] : -1;
+                    bool c = false, aj = false;
+                    if (j >= 0 && j != i && j != ex && ((livew[j >> 5] >> (j & 31)) & 1u)) {
+                        aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                        c = aj ? (mask & 1) : (mask & 2);
+                    }
+                    jv[u] = j;
+                    sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                    dv[u] = c ? __ldcs(drow + j) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
+            }
+        } else if (cnt[i] != 0u) {
+            // id-ordered walk, one bitset word per warp-iteration: lane l takes id
+            // 32 w + l, whose liveness and adjacency bits come from two broadcast words,
+            // and the D loads of a warp are one contiguous 256-byte row segment
             for (int w0 = 0; w0 < W; w0 += U) {
                 double dv[U];
-                uint32_t sel[U];  // bit0: candidate, bit1: adjacent
+                uint32_t sel[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int w = w0 + u;
@@ -855,38 +885,30 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     const bool aj = (aw >> lane) & 1u;
                     const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (mask & 1) : (mask & 2));
                     sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                    dv[u] = c ? __ldcs(drow + j) : kInf;
+                    dv[u] = c ? __ldcs(drow + j) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (!(sel[u] & 1u)) continue;
-                    const long long r = __double_as_longlong(dv[u]);
-                    C2x& x = (sel[u] & 2u) ? xa : xn;
-                    x.kmax = max(x.kmax, r < 0 ? (int)(r & 63) : 0);
-                    c2_put(x, __longlong_as_double(r & 0x7fffffffffffffffLL), ((w0 + u) << 5) + lane, dv[u]);
-                }
+                for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
             }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-            for (int st = 0; st < 2; ++st) {
-                C2x& x = st ? xn : xa;
-                const double c1 = __shfl_xor_sync(0xffffffffu, x.c1, o), v1 = __shfl_xor_sync(0xffffffffu, x.v1, o);
-                const double c2 = __shfl_xor_sync(0xffffffffu, x.c2, o);
-                const int j1 = __shfl_xor_sync(0xffffffffu, x.j1, o), km = __shfl_xor_sync(0xffffffffu, x.kmax, o);
-                x.kmax = max(x.kmax, km);
-                if (j1 != kNoJ) c2_put(x, c1, j1, v1);
-                if (c2 < x.c2) x.c2 = c2;
-            }
+            const unsigned long long oa1 = __shfl_xor_sync(0xffffffffu, a1, o), oa2 = __shfl_xor_sync(0xffffffffu, a2, o);
+            const unsigned long long on1 = __shfl_xor_sync(0xffffffffu, n1, o), on2 = __shfl_xor_sync(0xffffffffu, n2, o);
+            km = max(km, __shfl_xor_sync(0xffffffffu, km, o));
+            a2 = min(min(a2, oa2), max(a1, oa1));
+            a1 = min(a1, oa1);
+            n2 = min(min(n2, on2), max(n1, on1));
+            n1 = min(n1, on1);
         }
         int slow = 0;
-        if ((mask & 1) && xa.j1 != kNoJ && !c2_unique(xa)) slow |= 1;
-        if ((mask & 2) && xn.j1 != kNoJ && !c2_unique(xn)) slow |= 2;
+        double va = kInf, vn = kInf;
+        if ((mask & 1) && a1 != kKeyNone && !key_unique(a1, a2, km, drow, va)) slow |= 1;
+        if ((mask & 2) && n1 != kKeyNone && !key_unique(n1, n2, km, drow, vn)) slow |= 2;
         if (lane == 0) {
             const int r = i - lo;
-            if ((mask & 1) && !(slow & 1)) { bAd[r] = xa.v1; bAj[r] = xa.j1 == kNoJ ? -1 : xa.j1; }
-            if ((mask & 2) && !(slow & 2)) { bNd[r] = xn.v1; bNj[r] = xn.j1 == kNoJ ? -1 : xn.j1; }
+            if ((mask & 1) && !(slow & 1)) { bAd[r] = va; bAj[r] = a1 == kKeyNone ? -1 : (int)(a1 & 0x3fff); }
+            if ((mask & 2) && !(slow & 2)) { bNd[r] = vn; bNj[r] = n1 == kKeyNone ? -1 : (int)(n1 & 0x3fff); }
         }
         if (slow) rescanf_full(i, slow, ex);
     };
@@ -1504,7 +1526,15 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     __syncthreads();
                 }
             } else if (APO) {
-                for (int k = warp; k < ni; k += kWarps) rescanf(inv[k] >> 2, inv[k] & 3, a);
+                const long long tr0 = clock64();
+                int nr = 0;
+                for (int k = warp; k < ni; k += kWarps, ++nr) rescanf(inv[k] >> 2, inv[k] & 3, a);
+                if (bt.prof && lane == 0 && nr) {
+                    const unsigned long long dt = (unsigned long long)(clock64() - tr0);
+                    atomicAdd(bt.prof + 13, dt);             // warp-rescan cycles
+                    atomicAdd(bt.prof + 14, (unsigned long long)nr);  // rescans
+                    atomicMax(bt.prof + 15, dt);
+                }
             } else {
                 for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
             }

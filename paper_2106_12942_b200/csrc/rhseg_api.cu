@@ -471,6 +471,9 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
                     "%.2f rescan exact pairs (%.0f cycles each)\n", lv.level, (double)ph[8] / std::max(1LL, steps),
                     (double)ph[9] / std::max(1LL, steps), (double)ph[11] / std::max(1LL, steps),
                     (double)ph[12] / std::max(1ULL, ph[11]));
+        if (ph[14])
+            fprintf(stderr, "[rhseg profile] level %d APO rescans: %.0f cycles per rescan (warp view), max warp %.0f\n",
+                    lv.level, (double)ph[13] / ph[14], (double)ph[15]);
         cudaFree(prof);
         fprintf(stderr, "[rhseg profile] level %d host wall in run_level %.2f ms; per CTA: prologue %.0f cycles, "
                 "kernel %.0f cycles\n", lv.level, now_ms() - t_enter, (double)ph[6] / (lv.nsec * lv.C),

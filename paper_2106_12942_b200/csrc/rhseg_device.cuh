@@ -234,16 +234,19 @@ __device__ __forceinline__ void block_min_rb2(RowBest& a, RowBest& b, RowBest* s
         scratch[kWarps + warp] = b;
     }
     __syncthreads();
-    RowBest ra = scratch[0], rb = scratch[kWarps];
+    // lanes 0..7 combine the per-warp minima of a, lanes 8..15 those of b
+    RowBest r = lane < 2 * kWarps ? scratch[lane] : rb_none();
 #pragma unroll
-    for (int w = 1; w < kWarps; ++w) {
-        const RowBest c = scratch[w], d = scratch[kWarps + w];
-        if (c.d < ra.d || (c.d == ra.d && c.j < ra.j)) ra = c;
-        if (d.d < rb.d || (d.d == rb.d && d.j < rb.j)) rb = d;
+    for (int o = kWarps / 2; o > 0; o >>= 1) {
+        const double d = __shfl_xor_sync(0xffffffffu, r.d, o);
+        const int j = __shfl_xor_sync(0xffffffffu, r.j, o);
+        if (d < r.d || (d == r.d && j < r.j)) { r.d = d; r.j = j; }
     }
+    a.d = __shfl_sync(0xffffffffu, r.d, 0);
+    a.j = __shfl_sync(0xffffffffu, r.j, 0);
+    b.d = __shfl_sync(0xffffffffu, r.d, kWarps);
+    b.j = __shfl_sync(0xffffffffu, r.j, kWarps);
     __syncthreads();
-    a = ra;
-    b = rb;
 }
 
 // ---------------------------------------------------------------------------
