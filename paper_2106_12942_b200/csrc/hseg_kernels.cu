@@ -184,6 +184,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
 // per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
+#ifndef RHSEG_APO_OVERLAP
+#define RHSEG_APO_OVERLAP 0  // 1: row a' intervals by each warp right after its rescans (measured slower on C4)
+#endif
 #ifndef RHSEG_APO
 #define RHSEG_APO 1  // bound row a' from D (no mean stream) where possible; host may still disable
 #endif
@@ -1469,6 +1472,46 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         // offers (d(i, a), a) to every row) and b (dead). Their D loads overlap the
         // row-a stream already in flight.
         __syncthreads();
+        double apo_uA = kInf, apo_uN = kInf;  // this thread's smallest upper bounds of row a'
+        // APO: interval around every d(a', j) from the old D rows a and b (parallelogram
+        // identity, apo_interval), written to D; bounds kept per slot for the offers
+        auto apo_rows = [&]() {
+            double* sdl = reinterpret_cast<double*>(smem + L.sdv);
+            double* sdh = sdl + Rs;
+            const double* Da = D + (size_t)a * Rp;
+            const double* Db = D + (size_t)b * Rp;
+            constexpr int NQ = kMaxSlots / kThreads;
+            double ra[NQ], rb[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {  // all loads in flight first
+                const int sl = tid + q * kThreads;
+                const int j = sl < ss.S ? col[sl] : -1;
+                const bool ok = j >= 0 && j != a && j != b && cnt[j] != 0u;
+                ra[q] = ok ? __ldcg(Da + j) : 0.0;
+                rb[q] = ok ? __ldcg(Db + j) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int sl = tid + q * kThreads;
+                if (sl < ss.S) { sdl[sl] = ra[q]; sdh[sl] = rb[q]; }
+            }
+#pragma unroll 1
+            for (int sl = tid; sl < ss.S; sl += kThreads) {
+                const int j = col[sl];
+                if (j < 0 || j == a || j == b || cnt[j] == 0u) continue;
+                double dlo, dhi, v;
+                apo_interval<M>(ap, sdl[sl], sdh[sl], (double)cnt[j], dlo, dhi);
+                sdl[sl] = dlo;
+                sdh[sl] = dhi;
+                if ((sra[j >> 5] >> (j & 31)) & 1u) apo_uA = fmin(apo_uA, dhi);
+                else apo_uN = fmin(apo_uN, dhi);
+                if (d_pack_interval(dlo, dhi, v)) {  // (too wide: made exact after C2)
+                    D[(size_t)j * Rp + a] = v;
+                    D[(size_t)a * Rp + j] = v;
+                }
+            }
+        };
+        if (APO && tid == 0) { sScan = 0; misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
         {
             const int ni = ninv;
             if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
@@ -1529,6 +1572,9 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 const long long tr0 = clock64();
                 int nr = 0;
                 for (int k = warp; k < ni; k += kWarps, ++nr) rescanf(inv[k] >> 2, inv[k] & 3, a);
+                // then, without waiting for the other warps' rescans: the intervals of
+                // row a' (D rows a and b are not touched by the rescans, which skip a)
+                if (RHSEG_APO_OVERLAP) apo_rows();
                 if (bt.prof && lane == 0 && nr) {
                     const unsigned long long dt = (unsigned long long)(clock64() - tr0);
                     atomicAdd(bt.prof + 13, dt);             // warp-rescan cycles
@@ -1540,14 +1586,14 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             }
         }
         __syncthreads();
+        if (APO && !RHSEG_APO_OVERLAP) {
+            apo_rows();
+            __syncthreads();
+        }
         mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
         double n2a = 0.0;
-        if (APO) {
-            if (tid == 0) sScan = 0;
-            __syncthreads();
-        }
         if (M == kSam) {  // squared norm of a's new mean, sequential (oracle order)
             double* sn2a = reinterpret_cast<double*>(misc + 6);
             if (tid == 0) {
@@ -1603,64 +1649,18 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 ss.issued += max(0, ss.nst - NS);
             }
             if (APO) {
-                // an interval around every d(a', j) (from D rows a and b) goes to D;
-                // an offer is resolved exactly only when its lower bound reaches row j's
-                // (exact) cached best. a's own best: the exact lexicographic minimum of
-                // the columns whose lower bound reaches the stage's smallest upper bound.
-                const double* Da = D + (size_t)a * Rp;
-                const double* Db = D + (size_t)b * Rp;
-                double* sdl = reinterpret_cast<double*>(smem + L.sdv);  // per own slot: d(a, j) -> lower bound
-                double* sdh = sdl + Rs;                                 //               d(b, j) -> upper bound
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {  // all loads in flight first
-                    if (valid[q]) {
-                        const int sl = tid + q * kThreads;
-                        sdl[sl] = __ldcg(Da + jq[q]);
-                        sdh[sl] = __ldcg(Db + jq[q]);
-                    }
-                }
+                // (row a' intervals: apo_rows, run by each warp right after its rescans)
+                // offers: decided on the intervals unless they overlap row j's cached
+                // best (then both sides are made exact below); a's own best: the columns
+                // whose lower bound reaches the stage's smallest upper bound
+                double* sdl = reinterpret_cast<double*>(smem + L.sdv);
+                double* sdh = sdl + Rs;
                 int* cntF = misc + 10;  // offers that need the exact d(a', j)
-                if (tid == 0) { cntF[0] = 0; ak[6] = 0u; ak[7] = 0u; }
-                __syncthreads();
                 unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);  // exact offers
                 unsigned short* l2 = l1 + Rs;                                 // a's candidates
                 // (l1 and l2 each hold at most one entry per own column; entry = j |
                 // 0x4000 non-adjacent stage | 0x8000 interval too wide to store)
-                double uA = kInf, uN = kInf;
-#pragma unroll 1
-                for (int sl = tid; sl < ss.S; sl += kThreads) {
-                    const int j = col[sl];
-                    if (j < 0 || j == a || j == b || cnt[j] == 0u) continue;
-                    const bool aj = (sra[j >> 5] >> (j & 31)) & 1u;
-                    const int r = j - lo;
-                    double dlo, dhi;
-                    apo_interval<M>(ap, sdl[sl], sdh[sl], (double)cnt[j], dlo, dhi);
-                    sdl[sl] = dlo;
-                    sdh[sl] = dhi;
-                    if (aj) uA = fmin(uA, dhi);
-                    else uN = fmin(uN, dhi);
-                    const unsigned short e = (unsigned short)(j | (aj ? 0 : 0x4000));
-                    double v;
-                    if (!d_pack_interval(dlo, dhi, v)) {  // exact d(a', j) below, then the offer
-                        l1[atomicAdd(&cntF[0], 1)] = (unsigned short)(e | 0x8000);
-                        continue;
-                    }
-                    D[(size_t)j * Rp + a] = v;
-                    D[(size_t)a * Rp + j] = v;
-                    // offer (d(a', j), a) to row j: decided on the intervals unless they
-                    // overlap (then both sides are made exact below)
-                    double& bv = aj ? bAd[r] : bNd[r];
-                    int& bj = aj ? bAj[r] : bNj[r];
-                    if (bj < 0) {
-                        bv = v;
-                        bj = a;
-                    } else {
-                        double bl, bh;
-                        d_unpack(bv, bl, bh);
-                        if (dhi < bl) { bv = v; bj = a; }
-                        else if (!(dlo > bh)) l1[atomicAdd(&cntF[0], 1)] = e;
-                    }
-                }
+                double uA = apo_uA, uN = apo_uN;
                 {
                     RowBest x{uA, 0}, y{uN, 0};
                     block_min_rb2(x, y, rscr);
@@ -1672,9 +1672,28 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     const int j = col[sl];
                     if (j < 0 || j == a || j == b || cnt[j] == 0u) continue;
                     const bool aj = (sra[j >> 5] >> (j & 31)) & 1u;
-                    if (sdl[sl] <= (aj ? uA : uN)) {
-                        l2[atomicAdd(&sScan, 1)] = (unsigned short)(j | (aj ? 0 : 0x4000));
+                    const int r = j - lo;
+                    const double dlo = sdl[sl], dhi = sdh[sl];
+                    const unsigned short e = (unsigned short)(j | (aj ? 0 : 0x4000));
+                    if (dlo <= (aj ? uA : uN)) {
+                        l2[atomicAdd(&sScan, 1)] = e;
                         atomicAdd(&ak[aj ? 6 : 7], 1u);
+                    }
+                    double v;
+                    if (!d_pack_interval(dlo, dhi, v)) {  // exact d(a', j) below, then the offer
+                        l1[atomicAdd(&cntF[0], 1)] = (unsigned short)(e | 0x8000);
+                        continue;
+                    }
+                    double& bv = aj ? bAd[r] : bNd[r];
+                    int& bj = aj ? bAj[r] : bNj[r];
+                    if (bj < 0) {
+                        bv = v;
+                        bj = a;
+                    } else {
+                        double bl, bh;
+                        d_unpack(bv, bl, bh);
+                        if (dhi < bl) { bv = v; bj = a; }
+                        else if (!(dlo > bh)) l1[atomicAdd(&cntF[0], 1)] = e;
                     }
                 }
                 __syncthreads();
