@@ -405,7 +405,20 @@ def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
     loop_ms, dinit_ms = phases[2], phases[1]
     if loop_ms >= dinit_ms:
         # leaves dominate (>99% of steps at t=16); count leaf-level steps only
-        if w > 0:
+        resc = ctypes.c_int64(0)
+        _lib.check(_lib.load().rhseg_result_rescans(ctx.handle, levels, ctypes.byref(resc)), "rescans")
+        apo = w > 0 and MEASURE_OF.get(name) != "sam" and os.environ.get("RHSEG_APO", "1") != "0"
+        if apo:
+            # no mean stream: per step D rows a and b are read and row + column a' written
+            # (4 R 8 bytes), a's and b's band sums and a's new mean (4 B 8), plus every
+            # rescanned row's live D entries (rescans counted by the kernel x mean R)
+            steps = range(t + 1, R0 + 1)
+            per_sec = sum(4 * R * 8 + 4 * bands * 8 for R in steps)
+            rbar = sum(steps) / max(1, len(steps))
+            note = ("APO loop (latency/issue-bound step chain, not a stream): sum_steps (4R*8 + 4B*8) + "
+                    "rescans*mean(R)*8 bytes; %d leaf-level rescans" % resc.value)
+            per_sec += resc.value * rbar * 8 / nleaf
+        elif w > 0:
             per_sec = sum(R * (8 * bands + 16) for R in range(t + 1, R0 + 1))
             note = "streams the live regions' fp64 means once per step: sum_steps R_live*(8B+16)"
         else:  # adjacency only: a's neighbours' band sums (~8 on an 8-connected grid) + a's own

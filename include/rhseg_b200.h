@@ -181,6 +181,9 @@ int rhseg_result_phase_ms(rhseg_ctx *ctx, float *ms4);
 /* Kernels this library launched for the last run_* call, plus result copies
  * (rhseg_result_log) made since (the bench's gpu_launches evidence). */
 int rhseg_result_launches(rhseg_ctx *ctx, int64_t *n);
+/* Rows the merge loops of the last run rescanned from D (level <= 0: all levels) --
+ * the traffic model of the loop's roofline (bench.py). */
+int rhseg_result_rescans(rhseg_ctx *ctx, int32_t level, int64_t *n);
 /* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure
  * sub/mul/add loop over the whole GPU (roofline denominator). */
 int rhseg_fp64_peak(rhseg_ctx *ctx, double *ops_per_s);

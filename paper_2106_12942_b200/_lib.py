@@ -82,6 +82,7 @@ _SIGS = {
     "rhseg_scan_nonadjacent": [i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, vp],
     "rhseg_result_phase_ms": [vp, vp],
     "rhseg_result_launches": [vp, vp],
+    "rhseg_result_rescans": [vp, ctypes.c_int32, vp],
     "rhseg_format_float": [f64, vp, i32],
     "rhseg_sha256_hex": [vp, i64, vp],
     "rhseg_write_outputs_host": [ctypes.c_char_p, ctypes.c_char_p, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,

@@ -1134,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     if (SPEC && R0 > target) begin_stream();
 
     int a_prev = -1, step = 0, conv = 0;
-    long long pairs = 0;
+    long long pairs = 0, nresc = 0;  // (nresc: row rescans, the loop's D-row reads; thread 0)
     // optional per-phase cycle accounting (RHSEG_PROFILE=1): thread 0 of every CTA
     unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // (+ APO counters at prof[8..15])
     long long tmark = clock64();
@@ -1514,6 +1514,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         if (APO && tid == 0) { sScan = 0; misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
         {
             const int ni = ninv;
+            if (tid == 0) nresc += ni;
             if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
             if (TOP2) {
                 for (int k = warp; k < ni; k += kWarps) rescan2(inv[k] >> 2, inv[k] & 3, a);
@@ -1832,6 +1833,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             bt.nlog[sec] = step;
             bt.conv[sec] = conv;
             if (bt.pairs) bt.pairs[sec] = pairs;
+            if (bt.nresc) bt.nresc[sec] = nresc;
         }
     }
 }

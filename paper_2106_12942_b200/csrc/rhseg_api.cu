@@ -106,7 +106,7 @@ struct Level {
     bool imported = false;  // state received from other ranks: not part of this ctx's logs
     int measure = 0;        // 0 sqrt-bsmse, 1 euclidean, 2 sam
     std::vector<int> R0h, tgth, nlogh, convh;
-    std::vector<long long> pairsh;
+    std::vector<long long> pairsh, rescsh;
     SectionBatch sb{};
     void* keep = nullptr;
     void* work = nullptr;
@@ -259,7 +259,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     const size_t oR0 = take(ns * 4), oT = take(ns * 4), oCnt = take(ns * Rp * 4), oPar = take(ns * Rp * 4),
                  oAs = take(ns * npx * 4), oMap = take(ns * Rp * 4), oLa = take(ns * Rp * 4),
                  oLb = take(ns * Rp * 4), oLd = take(ns * Rp * 8), oLk = take(ns * Rp), oN = take(ns * 4),
-                 oCv = take(ns * 4), oPr = take(ns * 8), oN2 = take(lv.measure == 2 ? ns * Rp * 8 : 0);
+                 oCv = take(ns * 4), oPr = take(ns * 8), oRs = take(ns * 8), oN2 = take(lv.measure == 2 ? ns * Rp * 8 : 0);
     const size_t keep_bytes = o;
     {
         int rc = get_buf(c, kBufLevel + 2 * slot, keep_bytes, &lv.keep);
@@ -318,6 +318,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.nlog = reinterpret_cast<int*>(K + oN);
     b.conv = reinterpret_cast<int*>(K + oCv);
     b.pairs = reinterpret_cast<long long*>(K + oPr);
+    b.nresc = reinterpret_cast<long long*>(K + oRs);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
     b.mu2 = spec ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
@@ -448,9 +449,11 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
     lv.nlogh.resize(lv.nsec);
     lv.convh.resize(lv.nsec);
     lv.pairsh.resize(lv.nsec);
+    lv.rescsh.resize(lv.nsec);
     CK(cudaMemcpyAsync(lv.nlogh.data(), lv.sb.nlog, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.convh.data(), lv.sb.conv, 4 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(lv.pairsh.data(), lv.sb.pairs, 8 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(lv.rescsh.data(), lv.sb.nresc, 8 * (size_t)lv.nsec, cudaMemcpyDeviceToHost, st));
     unsigned long long ph[16] = {0};
     if (prof) CK(cudaMemcpyAsync(ph, prof, 16 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -904,6 +907,7 @@ int rhseg_run_upper(rhseg_ctx* c, const void* d_pack, int32_t top_level, int32_t
     lv.nlogh.assign(nlog, nlog + lv.nsec);
     lv.convh.assign(lv.nsec, 0);
     lv.pairsh.assign(lv.nsec, 0);
+    lv.rescsh.assign(lv.nsec, 0);
     lv.tgth.assign(lv.nsec, 1);
     int rpmax = 0;
     for (int r : lv.R0h) rpmax = std::max(rpmax, r);
@@ -939,6 +943,16 @@ int rhseg_result_info_get(rhseg_ctx* c, rhseg_result_info* info) {
 int rhseg_result_phase_ms(rhseg_ctx* c, float* ms4) {
     if (!c || !c->phases_valid) return fail(RHSEG_E_STATE, "no timed run");
     for (int p = 0; p < 4; ++p) ms4[p] = c->phase_ms[p];
+    return RHSEG_OK;
+}
+
+int rhseg_result_rescans(rhseg_ctx* c, int32_t level, int64_t* n) {
+    if (!c || !n) return fail(RHSEG_E_INVALID, "NULL argument");
+    long long t = 0;
+    for (auto& lv : c->levels)
+        if (!lv.imported && (level <= 0 || lv.level == level))
+            for (long long x : lv.rescsh) t += x;
+    *n = t;
     return RHSEG_OK;
 }
 

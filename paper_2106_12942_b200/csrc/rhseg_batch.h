@@ -58,6 +58,7 @@ struct SectionBatch {
     int* nlog;
     int* conv;
     long long* pairs;    // [nsec] reference-equivalent spectral pairs, sum_steps R(R-1)/2 - E
+    long long* nresc;    // [nsec] rows rescanned from D by the merge loop (traffic accounting)
     int sec0;            // first section covered by D (D is allocated per launch chunk)
     unsigned long long* prof;  // [5] per-phase cycles summed over CTAs (nullptr = off)
 
