@@ -1218,6 +1218,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     const int j = st ? bNj[r] : bAj[r];
                     if (!d_is_interval(st ? bNd[r] : bAd[r])) continue;
                     const double d = exact_pair(i, j);
+                    __syncwarp();
                     if (lane == 0) {
                         if (st) bNd[r] = d;
                         else bAd[r] = d;
@@ -1712,6 +1713,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     double db = aj ? bAd[r] : bNd[r];
                     const bool binterval = bj >= 0 && d_is_interval(db);
                     if (binterval) db = exact_pair(j, bj);
+                    __syncwarp();  // every lane has read row j's cache before lane 0 rewrites it
                     if (lane == 0) {
                         D[(size_t)j * Rp + a] = daj;
                         D[(size_t)a * Rp + j] = daj;
