@@ -31,6 +31,46 @@
 
 namespace rhseg {
 
+// D entries: an exact value is a non-negative double (sign bit clear); an interval
+// (APO sections only, see the APO section below) is [sign=1 | centre c with its low 6
+// mantissa bits replaced by k] = c (1 -/+ 2^(k-46)).
+constexpr double kU64 = 1.1102230246251565e-16;
+constexpr int kApoKMax = 45;  // widest encodable interval: c (1 -/+ 1/2)
+__device__ __forceinline__ bool d_is_interval(double v) { return __double_as_longlong(v) < 0; }
+__device__ __forceinline__ void d_decode(double c, int k, double& lo, double& hi) {
+    const double rho = __longlong_as_double((long long)(k - 46 + 1023) << 52);
+    lo = __dmul_rd(c, 1.0 - rho);  // 1 -/+ rho are exact for 2^-46 <= rho <= 1/2
+    hi = __dmul_ru(c, 1.0 + rho);
+}
+__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
+    const long long b = __double_as_longlong(v);
+    if (b < 0) d_decode(__longlong_as_double(b & 0x7fffffffffffffc0LL), (int)(b & 63), lo, hi);
+    else lo = hi = v;
+}
+// encode [lo, hi] (0 < lo <= hi < inf); false when the interval is too wide to encode
+__device__ __forceinline__ bool d_pack_interval(double lo, double hi, double& out) {
+    if (lo == hi) { out = lo; return true; }
+    if (!(lo > 0.0) || !(hi < kInf)) return false;
+    const long long cb = __double_as_longlong(0.5 * lo + 0.5 * hi) & 0x7fffffffffffffc0LL;
+    const double c = __longlong_as_double(cb);  // truncated centre
+    // first guess from the exponents of the half-width and the centre, then verify
+    // with the decoder itself (rarely more than one extra iteration)
+    const double w = fmax(hi - c, c - lo);
+    const int ew = (int)((__double_as_longlong(w) >> 52) & 0x7ff), ec = (int)((cb >> 52) & 0x7ff);
+    int k = max(0, ew - ec + 47);
+    for (; k <= kApoKMax; ++k) {
+        double l2, h2;
+        d_decode(c, k, l2, h2);
+        if (l2 <= lo && h2 >= hi) break;
+    }
+    if (k > kApoKMax) return false;
+    out = __longlong_as_double((long long)(0x8000000000000000ULL | (unsigned long long)cb | (unsigned long long)k));
+    return true;
+}
+#ifndef RHSEG_DINIT_FMA
+#define RHSEG_DINIT_FMA 1  // APO sections: fused-multiply-add all-pairs init into intervals
+#endif
+
 // ===========================================================================
 // 1. All-pairs D initialisation (the spectral-clustering all-pairs stage).
 //    64x64 pair tiles, 256 threads, 4x4 register blocking, bands staged through
@@ -40,7 +80,14 @@ namespace rhseg {
 constexpr int kTile = 64;
 constexpr int kKB = 16;
 
-template <int M>
+// IV (APO sections, BSMSE/Euclidean): the per-band step is fl(a - b) then one fused
+// multiply-add -- 2 FP64 ops instead of 3 -- and D receives an interval around the
+// reference's value instead of the value itself. Both sums accumulate the same rounded
+// differences t_b: s_ref = sum t_b^2 (1 + th), s_fma = sum t_b^2 (1 + th'), |th|, |th'| <=
+// (B + 1) u (nonnegative terms), so d_ref lies within (B + 4) u of the d formed from s_fma;
+// the interval is twice that. The loop treats D entries as intervals anyway (exact values
+// only where a comparison needs them), so the merge sequence is unchanged.
+template <int M, bool IV = false>
 __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) {
     const int sec = bt.sec0 + blockIdx.y;
     const int R0 = bt.R0[sec];
@@ -94,7 +141,14 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[p][q] = acc_step<M>(acc[p][q], a[p], b[q]);
+                for (int q = 0; q < 4; ++q) {
+                    if (IV) {
+                        const double t = __dsub_rn(a[p], b[q]);
+                        acc[p][q] = __fma_rn(t, t, acc[p][q]);
+                    } else {
+                        acc[p][q] = acc_step<M>(acc[p][q], a[p], b[q]);
+                    }
+                }
         }
         __syncthreads();
     }
@@ -108,6 +162,11 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
             if (i < R0 && j < R0) {
                 d = pair_finish<M>((double)cnt[i], (double)cnt[j], acc[p][q], M == kSam ? n2[i] : 0.0,
                                    M == kSam ? n2[j] : 0.0);
+                if (IV && d > 0.0) {
+                    const double rho = 2.0 * (bt.B + 4) * 1.1102230246251565e-16;
+                    double v;
+                    if (d_pack_interval(__dmul_rd(d, __dsub_rd(1.0, rho)), __dmul_ru(d, __dadd_ru(1.0, rho)), v)) d = v;
+                }
                 D[(size_t)i * Rp + j] = d;
             }
             sT[4 * ty + p][4 * tx + q] = d;
@@ -158,7 +217,9 @@ void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st) {
         const int nt = (R0max + kTile - 1) / kTile;
         dim3 grid(nt * (nt + 1) / 2, nrun);
         if (b.measure == kSam) dinit_dense_kernel<kSam><<<grid, kThreads, 0, st>>>(b);
+        else if (b.measure == kEuclid && b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kEuclid, true><<<grid, kThreads, 0, st>>>(b);
         else if (b.measure == kEuclid) dinit_dense_kernel<kEuclid><<<grid, kThreads, 0, st>>>(b);
+        else if (b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kBsmse, true><<<grid, kThreads, 0, st>>>(b);
         else dinit_dense_kernel<kBsmse><<<grid, kThreads, 0, st>>>(b);
     } else {
         dim3 grid((R0max + kThreads - 1) / kThreads, nrun);
@@ -374,39 +435,6 @@ struct Top2Lists {
 //        subtraction and sqrt is covered by the doubled slack; ||v|| <= 2 max||m||)
 //   sqrt(T') in [||v|| -+ ee], ee = 10u max||m|| (>= 3.02u max||m|| for e, + sqrt/sub rounding)
 //   d(a',j) = sqrt(C') sqrt(T') sqrt(1 + eps'),  widened by 2 (E/2 + 8u) relative.
-constexpr double kU64 = 1.1102230246251565e-16;
-constexpr int kApoKMax = 45;  // widest encodable interval: c (1 -/+ 1/2)
-__device__ __forceinline__ bool d_is_interval(double v) { return __double_as_longlong(v) < 0; }
-__device__ __forceinline__ void d_decode(double c, int k, double& lo, double& hi) {
-    const double rho = __longlong_as_double((long long)(k - 46 + 1023) << 52);
-    lo = __dmul_rd(c, 1.0 - rho);  // 1 -/+ rho are exact for 2^-46 <= rho <= 1/2
-    hi = __dmul_ru(c, 1.0 + rho);
-}
-__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
-    const long long b = __double_as_longlong(v);
-    if (b < 0) d_decode(__longlong_as_double(b & 0x7fffffffffffffc0LL), (int)(b & 63), lo, hi);
-    else lo = hi = v;
-}
-// encode [lo, hi] (0 < lo <= hi < inf); false when the interval is too wide to encode
-__device__ __forceinline__ bool d_pack_interval(double lo, double hi, double& out) {
-    if (lo == hi) { out = lo; return true; }
-    if (!(lo > 0.0) || !(hi < kInf)) return false;
-    const long long cb = __double_as_longlong(0.5 * lo + 0.5 * hi) & 0x7fffffffffffffc0LL;
-    const double c = __longlong_as_double(cb);  // truncated centre
-    // first guess from the exponents of the half-width and the centre, then verify
-    // with the decoder itself (rarely more than one extra iteration)
-    const double w = fmax(hi - c, c - lo);
-    const int ew = (int)((__double_as_longlong(w) >> 52) & 0x7ff), ec = (int)((cb >> 52) & 0x7ff);
-    int k = max(0, ew - ec + 47);
-    for (; k <= kApoKMax; ++k) {
-        double l2, h2;
-        d_decode(c, k, l2, h2);
-        if (l2 <= lo && h2 >= hi) break;
-    }
-    if (k > kApoKMax) return false;
-    out = __longlong_as_double((long long)(0x8000000000000000ULL | (unsigned long long)cb | (unsigned long long)k));
-    return true;
-}
 // Per-step constants of the row-a' pass (identical in every thread).
 struct ApoStep {
     double lam, mu, kt_lo, kt_hi;  // na/nn, nb/nn, lam mu T_ab (d(a, b) may be an interval)
