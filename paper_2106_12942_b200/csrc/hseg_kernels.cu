@@ -869,58 +869,73 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         unsigned long long a1 = kKeyNone, a2 = kKeyNone, n1 = kKeyNone, n2 = kKeyNone;
         int km = 0;  // widest interval code over both stages (only widens the test)
         constexpr int U = 8;
-        auto take = [&](double v, int j, bool c, bool aj) {
-            const unsigned long long r = (unsigned long long)__double_as_longlong(v);
-            km = max(km, (int)(r >> 63) * (int)(r & 63));
-            const unsigned long long key = c ? ((r & kKeyHi) | (unsigned long long)j) : kKeyNone;
-            const unsigned long long ka = aj ? key : kKeyNone, kn = aj ? kKeyNone : key;
-            a2 = min(a2, max(a1, ka));
-            a1 = min(a1, ka);
-            n2 = min(n2, max(n1, kn));
-            n1 = min(n1, kn);
-        };
-        if (cnt[i] != 0u && 2 * ss.S < R0) {
-            // sparse (most regions merged away): walk the compacted live-column list
-            for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
-                double dv[U];
-                int jv[U];
-                uint32_t sel[U];
+        // the walk is specialised on the stage mask: a single-stage rescan (the common
+        // case) tracks one pair of keys
+        auto walk = [&](auto MKC) {
+            constexpr int MK = decltype(MKC)::value;
+            auto take = [&](double v, int j, bool c, bool aj) {
+                const unsigned long long r = (unsigned long long)__double_as_longlong(v);
+                km = max(km, (int)(r >> 63) * (int)(r & 63));
+                const unsigned long long key = c ? ((r & kKeyHi) | (unsigned long long)j) : kKeyNone;
+                if (MK == 1 || MK == 3) {
+                    const unsigned long long ka = (MK == 1 || aj) ? key : kKeyNone;
+                    a2 = min(a2, max(a1, ka));
+                    a1 = min(a1, ka);
+                }
+                if (MK == 2 || MK == 3) {
+                    const unsigned long long kn = (MK == 2 || !aj) ? key : kKeyNone;
+                    n2 = min(n2, max(n1, kn));
+                    n1 = min(n1, kn);
+                }
+            };
+            if (2 * ss.S < R0) {
+                // sparse (most regions merged away): walk the compacted live-column list
+                for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                    double dv[U];
+                    int jv[U];
+                    uint32_t sel[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int sl = s0 + 32 * u + lane;
-                    const int j = sl < ss.S ? col[sl] : -1;
-                    bool c = false, aj = false;
-                    if (j >= 0 && j != i && j != ex && ((livew[j >> 5] >> (j & 31)) & 1u)) {
-                        aj = (arow[j >> 5] >> (j & 31)) & 1u;
-                        c = aj ? (mask & 1) : (mask & 2);
+                    for (int u = 0; u < U; ++u) {
+                        const int sl = s0 + 32 * u + lane;
+                        const int j = sl < ss.S ? col[sl] : -1;
+                        bool c = false, aj = false;
+                        if (j >= 0 && j != i && j != ex && ((livew[j >> 5] >> (j & 31)) & 1u)) {
+                            aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                            c = aj ? (MK & 1) : (MK & 2);
+                        }
+                        jv[u] = j;
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
                     }
-                    jv[u] = j;
-                    sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                    dv[u] = c ? __ldcs(drow + j) : 0.0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
                 }
+            } else {
+                // id-ordered walk, one bitset word per warp-iteration: lane l takes id
+                // 32 w + l, whose liveness and adjacency bits come from two broadcast
+                // words, and the D loads of a warp are one contiguous 256-byte segment
+                for (int w0 = 0; w0 < W; w0 += U) {
+                    double dv[U];
+                    uint32_t sel[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
-            }
-        } else if (cnt[i] != 0u) {
-            // id-ordered walk, one bitset word per warp-iteration: lane l takes id
-            // 32 w + l, whose liveness and adjacency bits come from two broadcast words,
-            // and the D loads of a warp are one contiguous 256-byte row segment
-            for (int w0 = 0; w0 < W; w0 += U) {
-                double dv[U];
-                uint32_t sel[U];
+                    for (int u = 0; u < U; ++u) {
+                        const int w = w0 + u;
+                        const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
+                        const int j = (w << 5) + lane;
+                        const bool aj = (aw >> lane) & 1u;
+                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (MK & 1) : (MK & 2));
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int w = w0 + u;
-                    const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
-                    const int j = (w << 5) + lane;
-                    const bool aj = (aw >> lane) & 1u;
-                    const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (mask & 1) : (mask & 2));
-                    sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                    dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
                 }
-#pragma unroll
-                for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
             }
+        };
+        if (cnt[i] != 0u) {
+            if (mask == 1) walk(std::integral_constant<int, 1>{});
+            else if (mask == 2) walk(std::integral_constant<int, 2>{});
+            else walk(std::integral_constant<int, 3>{});
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1161,6 +1176,17 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     if (CLUSTER) cluster_barrier();
     if (SPEC && R0 > target) begin_stream();
 
+    if (APO) {
+        unsigned* ak0 = reinterpret_cast<unsigned*>(smem + L.apk);
+        if (tid == 0) {
+            ninv = 0;
+            nnb = 0;
+            sScan = 0;
+            ak0[0] = ak0[1] = ak0[4] = ak0[5] = 0xffffffffu;
+            ak0[2] = ak0[3] = 0u;
+        }
+        __syncthreads();
+    }
     int a_prev = -1, step = 0, conv = 0;
     long long pairs = 0, nresc = 0;  // (nresc: row rescans, the loop's D-row reads; thread 0)
     // optional per-phase cycle accounting (RHSEG_PROFILE=1): thread 0 of every CTA
@@ -1188,21 +1214,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             // whose lower bound reaches the smallest upper bound; when those rows all
             // hold the same pair (typically rows i and j of the winning pair) it is the
             // winner, interval or not. Otherwise their intervals are made exact.
-            if (tid == 0) {
-                if (a_prev >= 0) {
-                    const int r = a_prev - lo;
-                    bAd[r] = rpart[0].d;
-                    bAj[r] = rpart[0].j == kNoJ ? -1 : rpart[0].j;
-                    bNd[r] = rpart[1].d;
-                    bNj[r] = rpart[1].j == kNoJ ? -1 : rpart[1].j;
-                }
-                ninv = 0;
-                nnb = 0;
-                sScan = 0;
-                ak[0] = ak[1] = ak[4] = ak[5] = 0xffffffffu;
-                ak[2] = ak[3] = 0u;
-            }
-            __syncthreads();
+            // (a_prev's caches and this scratch were set at the end of the last step,
+            // or before the loop)
             double uA = kInf, uN = kInf;
             for (int i = lo + tid; i < hi; i += kThreads) {
                 if (cnt[i] == 0u) continue;
@@ -1382,8 +1395,10 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         mark(1);
         // (C1) rows whose cached partner was a or b (rescanned in C2, after the
         // merge); their D rows are prefetched into L2 while the merge runs.
-        // The barrier publishes thread 0's update of a_prev's caches (above).
-        __syncthreads();
+        // The barrier publishes thread 0's update of a_prev's caches (above). (APO: those
+        // were published at the end of the last step, and the argmin's shared reads are
+        // fenced by its own barriers.)
+        if (!APO) __syncthreads();
         for (int i = lo + tid; i < hi; i += kThreads) {
             if (cnt[i] == 0u || i == a || i == b) continue;
             const int r = i - lo;
@@ -1499,8 +1514,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         // (C2) rows whose cached partner was a or b: rescan them from D now,
         // skipping a (its entries are refreshed by the row-a pass, which then
         // offers (d(i, a), a) to every row) and b (dead). Their D loads overlap the
-        // row-a stream already in flight.
-        __syncthreads();
+        // row-a stream already in flight. (APO: the merge's closing barrier suffices.)
+        if (!APO) __syncthreads();
         double apo_uA = kInf, apo_uN = kInf;  // this thread's smallest upper bounds of row a'
         // APO: interval around every d(a', j) from the old D rows a and b (parallelogram
         // identity, apo_interval), written to D; bounds kept per slot for the offers
@@ -1616,10 +1631,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             }
         }
         __syncthreads();
-        if (APO && !RHSEG_APO_OVERLAP) {
-            apo_rows();
-            __syncthreads();
-        }
+        if (APO && !RHSEG_APO_OVERLAP) apo_rows();  // (own slots only: the offers' reduction barrier follows)
         mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
@@ -1750,7 +1762,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         else { bNd[r] = take_a ? daj : db; bNj[r] = take_a ? a : bj; }
                     }
                 }
-                __syncthreads();
+                if (n1) __syncthreads();  // (uniform: n1 was read after a barrier)
                 // a's best per stage: a single candidate is the minimum as it is
                 // (interval or not); several are compared exactly
                 const int nA = ak[6], nN = ak[7];
@@ -1814,11 +1826,25 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             }
         }
         if (SPEC) block_min_rb2(pA, pN, rscr);
+        else pA = block_min_rb(pA, rscr);
         if (APO) {  // a's new mean becomes version R0 + step (the old one stays for the log)
             for (int k = tid; k < B; k += kThreads) mr[(size_t)(R0 + step) * B + k] = mua[k];
-            if (tid == 0) ver[a] = (unsigned short)(R0 + step);
+            if (tid == 0) {
+                ver[a] = (unsigned short)(R0 + step);
+                // a's fresh caches and the next argmin's scratch, published by the
+                // barrier closing this step (no barrier needed at the next step's start)
+                const int r = a - lo;
+                bAd[r] = pA.d;
+                bAj[r] = pA.j == kNoJ ? -1 : pA.j;
+                bNd[r] = pN.d;
+                bNj[r] = pN.j == kNoJ ? -1 : pN.j;
+                ninv = 0;
+                nnb = 0;
+                sScan = 0;
+                ak[0] = ak[1] = ak[4] = ak[5] = 0xffffffffu;
+                ak[2] = ak[3] = 0u;
+            }
         }
-        else pA = block_min_rb(pA, rscr);
         if (tid == 0) {
             rpart[0] = pA;
             rpart[1] = pN;
