@@ -564,6 +564,9 @@ struct StreamState {
 #ifndef RHSEG_MINBLOCKS
 #define RHSEG_MINBLOCKS 2
 #endif
+#ifndef RHSEG_RESCAN_U
+#define RHSEG_RESCAN_U 4  // APO rescans: D loads in flight per lane (C4 loop: 8 -> 427 ms, 4 -> 380, 2 -> 402, 1 -> 387)
+#endif
 #ifndef RHSEG_APO_MINBLOCKS
 #define RHSEG_APO_MINBLOCKS 2
 #endif
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         const double* drow = D + (size_t)i * Rp;
         unsigned long long a1 = kKeyNone, a2 = kKeyNone, n1 = kKeyNone, n2 = kKeyNone;
         int km = 0;  // widest interval code over both stages (only widens the test)
-        constexpr int U = 8;
+        constexpr int U = RHSEG_RESCAN_U;
         // the walk is specialised on the stage mask: a single-stage rescan (the common
         // case) tracks one pair of keys
         auto walk = [&](auto MKC) {
