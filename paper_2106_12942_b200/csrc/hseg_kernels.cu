@@ -564,6 +564,13 @@ struct StreamState {
 #ifndef RHSEG_MINBLOCKS
 #define RHSEG_MINBLOCKS 2
 #endif
+#ifndef RHSEG_SPARSE_NUM  // APO rescans walk the live-column list when S / R0 < NUM / DEN
+#define RHSEG_SPARSE_NUM 1
+#define RHSEG_SPARSE_DEN 2
+#endif
+#ifndef RHSEG_APO_COMPACT  // APO: compact the live-column list when holes >= S / K
+#define RHSEG_APO_COMPACT 8
+#endif
 #ifndef RHSEG_RESCAN_U
 #define RHSEG_RESCAN_U 4  // APO rescans: D loads in flight per lane (C4 loop: 8 -> 427 ms, 4 -> 380, 2 -> 402, 1 -> 387)
 #endif
@@ -891,7 +898,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     n1 = min(n1, kn);
                 }
             };
-            if (2 * ss.S < R0) {
+            if (RHSEG_SPARSE_DEN * ss.S < RHSEG_SPARSE_NUM * R0) {
                 // sparse (most regions merged away): walk the compacted live-column list
                 for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
                     double dv[U];
@@ -1086,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         // compact when holes >= 2 sqrt(S): balances the streamed holes (~1/sqrt(S) of
         // the bytes) against the copy cost (2 S B words every 2 sqrt(S) merges)
         if (!STREAM) {  // APO: only the column list (no mean columns) is compacted
-            if (ss.S >= 64 && ss.holes * 8 >= ss.S) compact();
+            if (ss.S >= 64 && ss.holes * RHSEG_APO_COMPACT >= ss.S) compact();
             return;
         }
         if (ss.S >= 64 && ss.holes * ss.holes >= RHSEG_COMPACT_K * ss.S) compact();
