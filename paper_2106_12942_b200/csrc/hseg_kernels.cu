@@ -22,6 +22,12 @@
 // of its merges without returning to the host: CTA r owns rows [r*Rs, (r+1)*Rs). The
 // single cross-CTA exchange per step is a 64-byte slot per CTA read through DSMEM after
 // one barrier.cluster (double-buffered by step parity).
+//
+// APO variant (the default for w > 0, BSMSE/Euclidean, one CTA per section): row a is
+// not recomputed from the means at all. D rows a and b bound every d(a', j) through the
+// parallelogram identity (see "APO" below), so D entries and row caches may hold
+// rigorous intervals; exact values are formed only where a comparison needs them, and
+// the log's values after the loop. Same merge sequence, far fewer bytes per step.
 #include <cuda_runtime.h>
 
 #include <type_traits>

@@ -7,7 +7,8 @@
 //   mu    [B][Rp]       f64   band-major mean cache        -- sums/count (Appendix A.3)
 //   mu2   [B][Rp]       f64   ping-pong copy: the merge loop keeps each CTA's live columns
 //                             compacted (ascending ids) in mu / mu2 and streams them
-//   D     [Rp][Rp]      f64   dissimilarity matrix, kept exact for every live pair
+//   D     [Rp][Rp]      f64   dissimilarity matrix (exact values; APO sections may hold
+//                             encoded intervals around them) for every live pair
 //                             (w > 0) or every adjacent pair (w = 0)
 //   sums  [C][Rp][B]    f64   band sums, one private copy per cluster CTA
 //   adj   [C][Rp][W]    u32   symmetric adjacency bitset, one private copy per CTA
