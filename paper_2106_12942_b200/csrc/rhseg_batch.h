@@ -5,8 +5,9 @@
 // Per section s (all arrays padded to Rp = roundup(R0max, 32) region slots):
 //   count [Rp]          u32   pixel counts (0 = dead)      -- graph.py:86-92 pixel_count
 //   mu    [B][Rp]       f64   band-major mean cache        -- sums/count (Appendix A.3)
-//   mu2   [B][Rp]       f64   ping-pong copy: the merge loop keeps each CTA's live columns
-//                             compacted (ascending ids) in mu / mu2 and streams them
+//   mu2   [B][Rp]       f64   stream loop: ping-pong copy (each CTA's live columns compacted,
+//                             ascending ids, in mu / mu2 and streamed); APO loop: [2 Rp][B]
+//                             versioned region-major means (row R0 + t = mean made by step t)
 //   D     [Rp][Rp]      f64   dissimilarity matrix (exact values; APO sections may hold
 //                             encoded intervals around them) for every live pair
 //                             (w > 0) or every adjacent pair (w = 0)
