@@ -577,6 +577,9 @@ struct StreamState {
 #ifndef RHSEG_APO_COMPACT  // APO: compact the live-column list when holes >= S / K
 #define RHSEG_APO_COMPACT 8
 #endif
+#ifndef RHSEG_RESCAN_PIPE
+#define RHSEG_RESCAN_PIPE 0  // APO rescans: software-pipelined row walk
+#endif
 #ifndef RHSEG_RESCAN_U
 #define RHSEG_RESCAN_U 4  // APO rescans: D loads in flight per lane (C4 loop: 8 -> 427 ms, 4 -> 380, 2 -> 402, 1 -> 387)
 #endif
@@ -930,9 +933,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 // id-ordered walk, one bitset word per warp-iteration: lane l takes id
                 // 32 w + l, whose liveness and adjacency bits come from two broadcast
                 // words, and the D loads of a warp are one contiguous 256-byte segment
-                for (int w0 = 0; w0 < W; w0 += U) {
-                    double dv[U];
-                    uint32_t sel[U];
+                auto issue = [&](int w0, double* dv, uint32_t* sel) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int w = w0 + u;
@@ -943,8 +944,28 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
                         dv[u] = c ? __ldcs(drow + j) : 0.0;
                     }
+                };
+                if (RHSEG_RESCAN_PIPE) {
+                    // software-pipelined: the next batch's loads are in flight while this
+                    // batch is folded into the keys
+                    double dv[U], dn[U];
+                    uint32_t sel[U], sn[U];
+                    issue(0, dv, sel);
+                    for (int w0 = 0; w0 < W; w0 += U) {
+                        if (w0 + U < W) issue(w0 + U, dn, sn);
 #pragma unroll
-                    for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+                        for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) { dv[u] = dn[u]; sel[u] = sn[u]; }
+                    }
+                } else {
+                    for (int w0 = 0; w0 < W; w0 += U) {
+                        double dv[U];
+                        uint32_t sel[U];
+                        issue(w0, dv, sel);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+                    }
                 }
             }
         };
