@@ -460,3 +460,31 @@ def test_config4_sampled_leaves_vs_oracle(oracle):
         assert np.array_equal(np.asarray(a), ref["log_survivor"])
         assert np.array_equal(np.asarray(b), ref["log_absorbed"])
         assert np.array_equal(np.asarray(d).view(np.uint64), ref["log_dissim"].view(np.uint64))
+
+
+@pytest.mark.parametrize("apo", ["0", "1"])
+def test_loop_variants_vs_oracle(apo, oracle, monkeypatch):
+    """Both merge-loop formulations of w > 0 single-CTA sections -- APO (row a' bounded
+    from D rows a and b, interval D/caches) and the mean stream (RHSEG_APO=0) -- equal the
+    oracle, on noisy, tie-heavy integer and large-magnitude cubes (wide intervals,
+    exact fallbacks) and both measures they cover."""
+    monkeypatch.setenv("RHSEG_APO", apo)
+    rng = np.random.default_rng(7 + int(apo))
+    cubes = [
+        rng.normal(0, 25, size=(12, 32, 32)).astype(np.float32),
+        rng.integers(0, 3, size=(7, 32, 32)).astype(np.float32),       # ties everywhere
+        (rng.normal(0, 1, size=(20, 16, 16)) * 1e6 + 3e7).astype(np.float32),  # |m| >> d
+        rng.integers(0, 2, size=(1, 16, 16)).astype(np.float32),        # one band
+    ]
+    try:
+        for k, s in enumerate(cubes):
+            for measure in ("sqrt-bsmse", "euclidean"):
+                oracle.set_measure(measure)
+                b, e = s.shape[0], s.shape[1]
+                img = rh.HyperImage(e, e, b, s)
+                res = rh.rhseg_run(img, rh.RhsegParams(rh.HsegParams(0.37, 4, measure), 2, 6))
+                ref = oracle.rhseg_run(s, 2, 0.37, 4, 6)
+                assert_log_equal(_flat(res), ref, f"cube {k} {measure} APO={apo}")
+                assert np.array_equal(res.labels.labels, ref["labels"])
+    finally:
+        oracle.set_measure("sqrt-bsmse")
