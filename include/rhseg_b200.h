@@ -45,6 +45,8 @@ extern "C" {
 #define RHSEG_E_CUDA 3        /* CUDA failure / no sm_100a device */
 #define RHSEG_E_TOO_LARGE 4   /* section exceeds the device limits (R0 > 16384 regions) */
 #define RHSEG_E_STATE 5       /* no result available / wrong call order */
+#define RHSEG_E_TOO_MANY_LABELS 6 /* errors.TooManyLabels: label above 65535 in a PGM (hsio.py:85-101) */
+#define RHSEG_E_IO 7          /* OSError: an output file cannot be opened or written */
 
 typedef struct rhseg_ctx rhseg_ctx;
 

@@ -48,6 +48,8 @@ def lib():
         L.oracle_run_leaf.restype = i64
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_set_threads.restype = None
+        L.oracle_set_incremental.argtypes = [ctypes.c_int]
+        L.oracle_set_incremental.restype = None
         L.oracle_set_measure.argtypes = [ctypes.c_int]
         L.oracle_set_measure.restype = None
         L.oracle_acos.argtypes = [ctypes.c_double]
@@ -62,6 +64,14 @@ def _p(a):
 
 def set_threads(n: int) -> None:
     lib().oracle_set_threads(int(n))
+
+
+def set_incremental(on: bool) -> None:
+    """Process-wide HSEG mode of every following call: False (default) = the literal
+    restatement (both per-row tables rebuilt every step, engine.py:309-342); True = the
+    exact incremental checker (cached D and per-row bests, sections of a level in
+    parallel) -- the same records bit for bit, affordable at the full BASELINE sizes."""
+    lib().oracle_set_incremental(1 if on else 0)
 
 
 MEASURE_CODES = {"sqrt-bsmse": 0, "euclidean": 1, "sam": 2}

@@ -38,6 +38,7 @@ from .errors import (
     RhsegError,
     SelfMerge,
     ShapeMismatch,
+    TooManyLabels,
 )
 from .graph import (
     LabelMap,
@@ -48,13 +49,23 @@ from .graph import (
     RegionGraph,
     dense_renumber,
     extract_labels,
+    init_from_presegmentation,
     init_region_graph,
     label_map_from_graph,
     merge_regions,
 )
 from .image import HyperImage
-from .recursive import B200Executor, RecordList, RhsegParams, RhsegResult, rhseg_run
-from .sections import SectionId, SectionTask, log_order, partition, section_side, total_sections
+from .recursive import (
+    B200Executor,
+    RecordList,
+    RhsegParams,
+    RhsegResult,
+    assemble_result,
+    rhseg_run,
+    run_leaf,
+    run_upper_levels,
+)
+from .sections import SectionId, SectionTask, log_order, partition, section_side, stitch, total_sections
 from .synth import GroundTruth, gen_synthetic
 
 __version__ = "0.1.0"

@@ -13,7 +13,7 @@ import threading
 
 import numpy as np
 
-from .errors import DeviceError, ExtensionMissing, IndivisibleImage
+from .errors import DeviceError, ExtensionMissing, IndivisibleImage, TooManyLabels
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RHSEG_LIB_PATH") or os.path.join(PKG, "_lib", "librhseg_b200.so")
@@ -24,6 +24,8 @@ RHSEG_E_INDIVISIBLE = 2
 RHSEG_E_CUDA = 3
 RHSEG_E_TOO_LARGE = 4
 RHSEG_E_STATE = 5
+RHSEG_E_TOO_MANY_LABELS = 6
+RHSEG_E_IO = 7
 
 i32, i64, f64, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -132,6 +134,10 @@ def check(status: int, what: str = "") -> None:
         raise ValueError(msg)
     if status == RHSEG_E_INDIVISIBLE:
         raise IndivisibleImage(msg)
+    if status == RHSEG_E_TOO_MANY_LABELS:
+        raise TooManyLabels(msg)
+    if status == RHSEG_E_IO:
+        raise OSError(msg)
     raise DeviceError(f"{what}: {msg} (status {status})")
 
 
@@ -187,8 +193,10 @@ def _current_device() -> int:
 def make_params(weight, target, section_target, levels, connectivity=8, measure=0, cluster=0):
     p = RhsegParamsC()
     p.spectral_weight = float(weight)
-    p.target_regions = int(target)
-    p.section_target_regions = int(section_target or 0)
+    # the C struct holds int32 targets: a larger target means "no merge" exactly as
+    # INT32_MAX does (no section has that many regions), so clamp instead of wrapping
+    p.target_regions = min(int(target), 2**31 - 1)
+    p.section_target_regions = min(int(section_target or 0), 2**31 - 1)
     p.levels = int(levels)
     p.connectivity = int(connectivity)
     p.measure = int(measure)

@@ -20,6 +20,10 @@
 
 #include "../../include/rhseg_b200.h"
 
+namespace rhseg {
+int set_error(int code, const char* msg);  // rhseg_api.cu: the thread-local rhseg_last_error()
+}
+
 namespace {
 
 // ---- SHA-256 (FIPS 180-4) ---------------------------------------------------
@@ -221,7 +225,11 @@ int rhseg_write_outputs_host(const char* pgm_path, const char* jsonl_path, int32
                              const int32_t* sec_row, const int32_t* sec_col, const int64_t* sec_count,
                              const int32_t* survivor, const int32_t* absorbed, const double* dissim,
                              const uint8_t* kind, char* content_hash_hex65, int64_t* jsonl_bytes) {
-    if (!pgm_path || !jsonl_path || !labels || width < 1 || height < 1) return RHSEG_E_INVALID;
+    using rhseg::set_error;
+    if (!pgm_path || !jsonl_path || !labels || width < 1 || height < 1)
+        return set_error(RHSEG_E_INVALID, "write_outputs: NULL path/labels or empty image");
+    if (n_sections < 0 || (n_sections > 0 && (!sec_level || !sec_row || !sec_col || !sec_count)))
+        return set_error(RHSEG_E_INVALID, "write_outputs: bad section arrays");
     // ---- PGM (hsio.py:85-101) ----
     const size_t npx = (size_t)width * height;
     std::string pgm = "P5\n" + std::to_string(width) + " " + std::to_string(height) + "\n65535\n";
@@ -229,7 +237,11 @@ int rhseg_write_outputs_host(const char* pgm_path, const char* jsonl_path, int32
     pgm.resize(hdr + 2 * npx);
     for (size_t i = 0; i < npx; ++i) {
         const int32_t v = labels[i];
-        if (v < 0 || v > 65535) return RHSEG_E_INVALID;  // TooManyLabels in the reference
+        if (v < 0 || v > 65535) {  // hsio.py:88-92
+            char m[96];
+            snprintf(m, sizeof m, "label %d does not fit a 16-bit PGM (max 65535)", (int)v);
+            return set_error(RHSEG_E_TOO_MANY_LABELS, m);
+        }
         pgm[hdr + 2 * i] = (char)(v >> 8);
         pgm[hdr + 2 * i + 1] = (char)(v & 0xff);
     }
@@ -266,21 +278,27 @@ int rhseg_write_outputs_host(const char* pgm_path, const char* jsonl_path, int32
         });
     }
     for (auto& th : pool) th.join();
-    FILE* f = fopen(pgm_path, "wb");
-    if (!f) return RHSEG_E_INVALID;
-    fwrite(pgm.data(), 1, pgm.size(), f);
-    fclose(f);
-    f = fopen(jsonl_path, "wb");
-    if (!f) return RHSEG_E_INVALID;
+    // both files are opened before either is written, so a bad path leaves no partial set
+    FILE* fp = fopen(pgm_path, "wb");
+    if (!fp) return set_error(RHSEG_E_IO, (std::string("cannot open ") + pgm_path).c_str());
+    FILE* f = fopen(jsonl_path, "wb");
+    if (!f) {
+        fclose(fp);
+        remove(pgm_path);
+        return set_error(RHSEG_E_IO, (std::string("cannot open ") + jsonl_path).c_str());
+    }
+    bool ok = fwrite(pgm.data(), 1, pgm.size(), fp) == pgm.size();
+    ok &= fclose(fp) == 0;
     Sha256 h;
     h.update(pgm.data(), pgm.size());
     int64_t bytes = 0;
     for (auto& p : parts) {
-        fwrite(p.data(), 1, p.size(), f);
+        ok &= fwrite(p.data(), 1, p.size(), f) == p.size();
         h.update(p.data(), p.size());
         bytes += (int64_t)p.size();
     }
-    fclose(f);
+    ok &= fclose(f) == 0;
+    if (!ok) return set_error(RHSEG_E_IO, "short write of the output files");
     if (content_hash_hex65) {
         h.hex(content_hash_hex65);
         content_hash_hex65[64] = 0;

@@ -82,6 +82,10 @@ static int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+// for the library's other translation units (outputs.cu)
+namespace rhseg {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace rhseg
 #define CK(expr)                                                                            \
     do {                                                                                    \
         cudaError_t e_ = (expr);                                                            \
@@ -90,6 +94,9 @@ static int fail(int code, const std::string& msg) {
     } while (0)
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+// Largest section the merge loop supports: region ids are stored as 14-bit fields in
+// the loop kernel's shared-memory lists and keys (hseg_kernels.cu).
+constexpr long long kMaxSectionRegions = 16384;
 
 #ifndef RHSEG_L2_PERSIST_MB
 #define RHSEG_L2_PERSIST_MB 0  // off: no gain on C2, C4 3% slower with a 64 MB set-aside
@@ -221,8 +228,9 @@ static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced) {
 static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, int forced_C, int slot) {
     lv.R0max = 0;
     for (int r : lv.R0h) lv.R0max = std::max(lv.R0max, r);
-    if (lv.R0max > 16384)
-        return fail(RHSEG_E_TOO_LARGE, "section with " + std::to_string(lv.R0max) + " regions exceeds 16384");
+    if (lv.R0max > kMaxSectionRegions)
+        return fail(RHSEG_E_TOO_LARGE, "section with " + std::to_string(lv.R0max) + " regions exceeds " +
+                                           std::to_string(kMaxSectionRegions));
     lv.Rp = std::max(64, (lv.R0max + 63) / 64 * 64);
     lv.W = lv.Rp / 32;
     lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
@@ -571,6 +579,26 @@ static int validate(const rhseg_params* p, int edge, int bands) {
     if (p->cluster != 0 && p->cluster != 1 && p->cluster != 2 && p->cluster != 4 && p->cluster != 8 &&
         p->cluster != 16)
         return fail(RHSEG_E_INVALID, "cluster must be 0 (auto) or one of 1,2,4,8,16");
+    // Worst-case section sizes, checked before anything is launched: a leaf holds e*e
+    // regions and a parent the live regions of its four children, at most
+    // 4 * min(child size, section target) -- image sections are connected grids, so no
+    // section stops above its target (RHSEG_E_TOO_LARGE is a documented deviation).
+    {
+        const long long e = edge / side, sect = p->section_target_regions > 0 ? p->section_target_regions
+                                                                            : p->target_regions;
+        long long R = e * e;
+        if (R > kMaxSectionRegions)
+            return fail(RHSEG_E_TOO_LARGE, "leaf sections of " + std::to_string(e) + "x" + std::to_string(e) +
+                                               " pixels exceed " + std::to_string(kMaxSectionRegions) + " regions");
+        for (int level = p->levels - 1; level >= 1; --level) {
+            R = 4 * std::min(R, sect);
+            if (R > kMaxSectionRegions)
+                return fail(RHSEG_E_TOO_LARGE, "level-" + std::to_string(level) + " sections can hold " +
+                                                   std::to_string(R) + " regions (section_target_regions " +
+                                                   std::to_string(sect) + "), above the " +
+                                                   std::to_string(kMaxSectionRegions) + "-region section limit");
+        }
+    }
     return RHSEG_OK;
 }
 
@@ -678,7 +706,8 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     const int sect = p->section_target_regions > 0 ? p->section_target_regions : p->target_regions;
     const int side = 1 << (L - 1);
     const int e = edge / side;
-    if ((long long)e * e > 16384) return fail(RHSEG_E_TOO_LARGE, "leaf sections above 128x128 pixels are not supported");
+    if ((long long)e * e > kMaxSectionRegions)
+        return fail(RHSEG_E_TOO_LARGE, "leaf sections above 128x128 pixels are not supported");
     c->levels.reserve(L);
     // ---- leaves ----
     {
@@ -1141,7 +1170,8 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
         return fail(RHSEG_E_INVALID, "unknown measure; available: ['euclidean', 'sam', 'sqrt-bsmse']");
     if (target < 1) return fail(RHSEG_E_INVALID, "target_regions must be >= 1");
     if (n < 0 || nbands < 1) return fail(RHSEG_E_INVALID, "bad graph shape");
-    if (n > 16384) return fail(RHSEG_E_TOO_LARGE, "graph exceeds 16384 regions");
+    if (n > kMaxSectionRegions)
+        return fail(RHSEG_E_TOO_LARGE, "graph exceeds " + std::to_string(kMaxSectionRegions) + " regions");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
     reset_ctx(c, st);

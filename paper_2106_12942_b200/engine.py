@@ -274,9 +274,13 @@ def hseg_run(graph, params, strategy=Sequential(), profile: ProfileStats | None 
              device: int | None = None, cluster: int = 0):
     """Merge until target_regions remain (engine.py:345-371), on the device.
 
-    The whole loop runs in one persistent kernel; there is no per-step host
-    round trip, so `stop_check` is polled once before the device run (a
-    scheduler handoff point, engine.py:351-363)."""
+    The whole loop runs in one persistent kernel (no per-step host round trip).
+    `stop_check` keeps the reference's contract exactly (engine.py:351-363): it is
+    called before every step, with the caller's graph at that step boundary, and a
+    True ends the run with `interrupted` set. That is possible without stopping the
+    device because the merge sequence does not depend on when a run stops -- the
+    reference's interrupted run is a prefix of the full one -- so the device computes
+    the whole log and the host applies it one merge per stop_check."""
     t0 = time.perf_counter_ns()
     Hier, Kind, merge = _graph_api(graph)
     resolve_measure(params.measure)
@@ -300,21 +304,32 @@ def hseg_run(graph, params, strategy=Sequential(), profile: ProfileStats | None 
                 _lib.check(
                     _lib.load().rhseg_hseg_graph(
                         ctx.handle, n, nb, _lib.ptr(snap.counts), _lib.ptr(np.ascontiguousarray(snap.sums)),
-                        _lib.ptr(snap.indptr), _lib.ptr(snap.indices), float(params.spectral_weight), target,
-                        int(cluster), MEASURE_CODES[params.measure], _lib.ptr(sa), _lib.ptr(sb), _lib.ptr(sd), _lib.ptr(sk), ctypes.byref(nrec),
-                        ctypes.byref(conv),
+                        _lib.ptr(snap.indptr), _lib.ptr(snap.indices), float(params.spectral_weight),
+                        min(target, 2**62), int(cluster), MEASURE_CODES[params.measure], _lib.ptr(sa),
+                        _lib.ptr(sb), _lib.ptr(sd), _lib.ptr(sk), ctypes.byref(nrec), ctypes.byref(conv),
                     ),
                     "rhseg_hseg_graph",
                 )
                 dev_ms = _phase_ms(ctx)
             ids = snap.ids
+            applied = 0
             for k in range(nrec.value):
+                # the first step's check already ran above
+                if k > 0 and stop_check is not None and stop_check():
+                    hierarchy.interrupted = True
+                    break
                 hierarchy.records.append(
                     merge(graph, int(ids[sa[k]]), int(ids[sb[k]]), float(sd[k]), Kind(int(sk[k])))
                 )
-            hierarchy.converged_early = bool(conv.value)
+                applied += 1
+            if not hierarchy.interrupted and conv.value:
+                # the reference checks once more before the step that finds no pair
+                if applied > 0 and stop_check is not None and stop_check():
+                    hierarchy.interrupted = True
+                else:
+                    hierarchy.converged_early = True
             if profile is not None:
-                profile.steps += nrec.value
+                profile.steps += applied
                 profile.dissim_ns += int((dev_ms[1] + dev_ms[2]) * 1e6)
     if profile is not None:
         profile.total_ns += time.perf_counter_ns() - t0

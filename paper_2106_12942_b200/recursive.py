@@ -18,9 +18,10 @@ import numpy as np
 
 from . import _lib
 from .dissim import MEASURE_CODES
-from .engine import HsegParams, ProfileStats, Sequential, _phase_ms
-from .graph import LabelMap, MergeHierarchy, MergeKind, MergeRecord, RegionGraph, extract_labels
-from .sections import SectionId, check_divisible, log_order, section_side
+from .engine import HsegParams, ProfileStats, Sequential, _phase_ms, hseg_run
+from .graph import (LabelMap, MergeHierarchy, MergeKind, MergeRecord, RegionGraph, extract_labels,
+                    label_map_from_graph)
+from .sections import SectionId, check_divisible, log_order, section_side, stitch
 
 
 @dataclass
@@ -68,9 +69,17 @@ class RecordList(Sequence):
         return MergeRecord(i, int(self._a[i]), int(self._b[i]), float(self._d[i]), MergeKind(int(self._k[i])))
 
     def __eq__(self, other):
+        """Field by field, so a list of the reference's own MergeRecord objects (another
+        class with the same fields, graph.py:41-47) compares equal to the same records."""
         try:
-            return len(self) == len(other) and all(x == y for x, y in zip(self, other))
-        except TypeError:
+            if len(self) != len(other):
+                return False
+            return all(
+                (x.step, x.survivor_id, x.absorbed_id, x.dissimilarity, int(x.kind))
+                == (y.step, y.survivor_id, y.absorbed_id, y.dissimilarity, int(y.kind))
+                for x, y in zip(self, other)
+            )
+        except (TypeError, AttributeError):
             return NotImplemented
 
     def arrays(self):
@@ -245,6 +254,48 @@ def collect_result(ctx, info, edge: int, bands: int, levels: int) -> RhsegResult
     )
 
 
+def run_leaf(task, params: RhsegParams, strategy=Sequential(), connectivity: int = 8,
+             profile: ProfileStats | None = None):
+    """recursive.py:130-142: one leaf section (its HSEG on the device through the B2
+    seam); returns (graph, records, converged_early, pre-merge copy if the leaf is the
+    root)."""
+    from .graph import init_region_graph
+
+    graph = init_region_graph(task.image, connectivity)
+    root_initial = graph.copy() if task.section_id.level == 1 else None
+    hier = hseg_run(graph, params.section_params(task.section_id), strategy, profile)
+    return graph, hier.records, hier.converged_early, root_initial
+
+
+def run_upper_levels(params: RhsegParams, strategy, connectivity: int, graphs: dict, logs: dict,
+                     profile: ProfileStats | None = None):
+    """recursive.py:145-170: stitch and HSEG every level above the leaves (each section
+    on the device), mutating `graphs` and `logs`; returns (root_initial, converged_early)."""
+    converged_early, root_initial = False, None
+    for level in range(params.levels - 1, 0, -1):
+        side = section_side(level)
+        for r in range(side):
+            for c in range(side):
+                sid = SectionId(level, r, c)
+                graph = stitch([graphs[k] for k in sid.children()], connectivity)
+                if level == 1:
+                    root_initial = graph.copy()
+                hier = hseg_run(graph, params.section_params(sid), strategy, profile)
+                converged_early |= hier.converged_early
+                graphs[sid] = graph
+                logs[sid] = hier.records
+    return root_initial, converged_early
+
+
+def assemble_result(params: RhsegParams, logs: dict, root_initial, root_graph, converged_early: bool) -> RhsegResult:
+    """recursive.py:107-127: logs in log_order, the root's hierarchy and dense labels."""
+    ordered = [(sid, logs[sid]) for sid in log_order(params.levels)]
+    hierarchy = MergeHierarchy(initial_region_count=root_initial.live_count,
+                               records=list(logs[SectionId(1, 0, 0)]), converged_early=converged_early)
+    return RhsegResult(section_logs=ordered, root_initial=root_initial, root_hierarchy=hierarchy, graph=root_graph,
+                       labels=label_map_from_graph(root_graph), converged_early=converged_early)
+
+
 def rhseg_run(image, params: RhsegParams, strategy=Sequential(), executor=None,
               profile: ProfileStats | None = None) -> RhsegResult:
     """recursive.py:212-223; the default executor is the B200 one."""
@@ -255,5 +306,5 @@ def rhseg_run(image, params: RhsegParams, strategy=Sequential(), executor=None,
 
 __all__ = [
     "RhsegParams", "RhsegResult", "RecordList", "B200Executor", "rhseg_run", "log_order", "section_side",
-    "collect_result", "result_info",
+    "collect_result", "result_info", "run_leaf", "run_upper_levels", "assemble_result",
 ]

@@ -8,7 +8,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .errors import IndivisibleImage
+import numpy as np
+
+from .errors import IndivisibleImage, ShapeMismatch
 from .image import HyperImage
 
 
@@ -73,3 +75,49 @@ def log_order(levels: int) -> list[SectionId]:
         for r in range(section_side(level))
         for c in range(section_side(level))
     ]
+
+
+def stitch(quadrants, connectivity: int = 8):
+    """sections.py:103-163 as a host helper on RegionGraph objects (the device path
+    stitches whole levels in stitch_kernel): NW, NE, SW, SE children renumbered densely
+    (each child's live ids ascending, children in order), sums and counts carried over
+    exactly, and every pixel adjacency across the two internal seams linked."""
+    from .graph import Region, RegionGraph, neighbor_offsets
+
+    if len(quadrants) != 4:
+        raise ShapeMismatch(f"stitch needs exactly 4 quadrants, got {len(quadrants)}")
+    e, bands = quadrants[0].width, quadrants[0].bands
+    for g in quadrants:
+        if g.width != e or g.height != e:
+            raise ShapeMismatch("quadrants differ in size")
+        if g.bands != bands:
+            raise ShapeMismatch("quadrants differ in band count")
+    neighbor_offsets(connectivity)  # validates
+    n = 2 * e
+    out = RegionGraph(n, n, bands)
+    grid = np.empty((n, n), np.int64)
+    base = 0
+    for k, g in enumerate(quadrants):
+        ids = np.array(sorted(g.regions), np.int64)
+        orow, ocol = (k // 2) * e, (k % 2) * e
+        local = np.asarray(g.pixel_assignment, np.int64).reshape(e, e)
+        grid[orow:orow + e, ocol:ocol + e] = base + np.searchsorted(ids, local)
+        remap = {int(r): base + i for i, r in enumerate(ids.tolist())}
+        for rid, i in remap.items():
+            reg = g.regions[rid]
+            p = np.asarray(reg.pixels, np.int64)
+            out.regions[i] = Region(i, reg.pixel_count, reg.band_sums.copy(), {remap[a] for a in reg.adjacency},
+                                    ((orow + p // e) * n + ocol + p % e).tolist())
+        base += len(ids)
+    out.pixel_assignment = grid.reshape(-1).copy()
+    # seams: column e-1 | e and row e-1 | e, plus both diagonals across each under 8-connectivity
+    pairs = [(grid[:, e - 1], grid[:, e]), (grid[e - 1, :], grid[e, :])]
+    if connectivity == 8:
+        pairs += [(grid[:-1, e - 1], grid[1:, e]), (grid[:-1, e], grid[1:, e - 1]),
+                  (grid[e - 1, :-1], grid[e, 1:]), (grid[e - 1, 1:], grid[e, :-1])]
+    for a, b in pairs:
+        m = a != b
+        for x, y in zip(a[m].tolist(), b[m].tolist()):
+            out.regions[x].adjacency.add(y)
+            out.regions[y].adjacency.add(x)
+    return out

@@ -70,3 +70,26 @@ def test_native_jsonl_equals_reference_bytes(name, tmp_path):
     pgm = f"P5\n{labels.shape[1]} {labels.shape[0]}\n65535\n".encode() + labels.astype(">u2").tobytes()
     assert (tmp_path / "x.pgm").read_bytes() == pgm
     assert out["content_hash"] == hashlib.sha256(pgm + jsonl).hexdigest()
+
+
+def _tiny_result(labels):
+    recs = RecordList(np.array([0], np.int32), np.array([1], np.int32), np.array([1.5]), np.array([0], np.uint8))
+    lab = np.asarray(labels)
+    return RhsegResult([(SectionId(1, 0, 0), recs)], None, None, None, LabelMap(lab.shape[1], lab.shape[0], lab))
+
+
+def test_write_outputs_errors_map_to_reference_types(tmp_path):
+    """A label above 65535 raises TooManyLabels (hsio.py:88-92) with a message and
+    writes nothing; an unopenable path raises OSError and leaves no partial file set."""
+    from paper_2106_12942_b200 import TooManyLabels
+
+    big = _tiny_result([[0, 70000], [1, 2]])
+    with pytest.raises(TooManyLabels, match="70000"):
+        outputs.write_outputs(big, tmp_path / "a.pgm", tmp_path / "a.merges.jsonl")
+    assert not (tmp_path / "a.pgm").exists() and not (tmp_path / "a.merges.jsonl").exists()
+    ok = _tiny_result([[0, 1], [1, 2]])
+    with pytest.raises(OSError, match="cannot open"):
+        outputs.write_outputs(ok, tmp_path / "b.pgm", tmp_path / "missing_dir" / "b.merges.jsonl")
+    assert not (tmp_path / "b.pgm").exists()
+    out = outputs.write_outputs(ok, tmp_path / "c.pgm", tmp_path / "c.merges.jsonl")
+    assert len(out["content_hash"]) == 64
