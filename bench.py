@@ -62,6 +62,17 @@ UNIT = "pixel-bands/s"
 L2_BYTES = 126 * 1024 * 1024
 
 
+def config_of(name):
+    """The workload's config dict -- identical in both arms (the driver compares them);
+    arm-specific execution details go to the line's top-level "execution" key."""
+    spec, crop, levels, w, t, st = WORKLOADS[name]
+    bands, edge, _ = cube_shape(name)
+    return {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels, "spectral_weight": w,
+            "target_regions": t, "section_target_regions": st, "connectivity": 8,
+            "measure": MEASURE_OF.get(name, "sqrt-bsmse"),
+            "l2": "flushed between timed steps (2x126 MB write); CPU arm: n/a"}
+
+
 def make_cube(name, out=None):
     from paper_2106_12942_b200.synth import gen_synthetic
 
@@ -185,6 +196,29 @@ def cpu_sample(name, samples, seconds_hint=20.0, threads=None, max_leaves=None, 
     }
 
 
+def full_cpu_plan(name):
+    """The BASELINE.md §4 plan measured once on the box's host (tools/cpu_baseline.py:
+    >= 2 x ncores leaves, within-leaf OpenMP vs one leaf per core, the faster kept),
+    committed as profiles/r02_cpu_baseline.jsonl; None if this workload was not run."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_cpu_baseline.jsonl")) as f:
+            rows = [json.loads(x) for x in f if x.strip()]
+    except OSError:
+        return None
+    for r in rows:
+        if r.get("workload") == name:
+            out = {"source": "profiles/r02_cpu_baseline.jsonl", "cores": r["cores"], "value": r["value"],
+                   "unit": UNIT}
+            if "best" in r:
+                out.update(best=r["best"], leaves=f"{r['leaves_sampled']}/{r['leaves_total']}",
+                           within=r["within"]["pixel_bands_per_s"], sections=r["sections"]["pixel_bands_per_s"],
+                           extrapolated=r["extrapolated"])
+            if "single_core" in r:
+                out["single_core"] = r["single_core"]["pixel_bands_per_s"]
+            return out
+    return None
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -214,8 +248,9 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
-        "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "connectivity": 8,
-                   "parallelism": "cpu-openmp", "l2": "n/a (CPU)"},
+        "config": config_of(name),
+        "execution": f"CPU (no GPU): the reference algorithm restated in C (oracle/), OpenMP over "
+                     f"{last['cores']} host threads, bounded random leaf sample",
         "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": value},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -241,7 +276,7 @@ def run_ours(args):
     if world > 1:
         from paper_2106_12942_b200 import distributed as rdist
 
-        return rdist.bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, cpu_sample)
+        return rdist.bench_sharded(args, sys.modules[__name__])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -317,7 +352,7 @@ def run_ours(args):
     d2h = n_rec * (4 + 4 + 8 + 1) + edge * edge * 4
 
     # ---- roofline of the dominant kernel ----
-    roof = roofline(name, edge, bands, levels, w, phases, info, ex, ctx)
+    roof, roof2 = roofline(name, edge, bands, levels, w, phases, ctx.handle)
 
     line = {
         "metric": METRIC,
@@ -332,11 +367,8 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
-        "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels,
-                   "spectral_weight": w, "target_regions": t, "connectivity": 8,
-                   "measure": MEASURE_OF.get(name, "sqrt-bsmse"),
-                   "parallelism": "1 GPU, every section of a level concurrent",
-                   "l2": "flushed between timed steps (2x126 MB write)"},
+        "config": config_of(name),
+        "execution": "1 GPU, every section of a quadtree level in one persistent launch",
         "spectral_pairs_per_s": pairs / (ms * 1e-3),
         "merges": n_rec,
         "host_wall_ms_per_step": float(np.mean(walls)) * 1e3,
@@ -346,11 +378,15 @@ def run_ours(args):
         "e2e": {"value": npxb / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3},
         "roofline": roof,
+        "roofline_secondary": roof2,
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
         cb = cpu_sample(name, host.numpy(), seconds_hint=args.ref_seconds)
         line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        fp = full_cpu_plan(name)
+        if fp:
+            line["cpu_baseline"]["full_plan"] = fp
     print(json.dumps(line), flush=True)
     return 0
 
@@ -384,67 +420,68 @@ def ncu_traffic(name, kernel):
     return None if not t else t["dram_read_bytes"] + t["dram_write_bytes"]
 
 
-def roofline(name, edge, bands, levels, w, phases, info, ex, ctx):
-    """Dominant kernel = the longer of the merge loop (phase 2) and the
-    all-pairs D init (phase 1). Algorithmic work per DESIGN.md §4:
-      dinit (FP64 pipe): sum over sections of R0(R0+1)/2 pairs x (3B+5) ops;
-      merge loop (HBM): per step the row-a pass streams the live regions'
-      fp64 mean vectors once: sum_steps R_live * B * 8 bytes (+ D row/col
-      updates 2*R*8), i.e. ~ sum over sections sum_{R=t+1..R0} R*(8B+16)."""
+def roofline(name, edge, bands, levels, w, phases, handle, leaf=None):
+    """Roofline entries of the two heavy kernels; the longer one is the line's
+    `roofline` (DESIGN.md §4 states the per-unit algorithmic work):
+      merge loop (HBM): the leaf level's loop -- the variant that ACTUALLY ran
+        (rhseg_result_level_info), >99% of the merges at t=16:
+          APO:    per step D rows a and b read, row and column a' written (4 R 8 bytes),
+                  a's and b's band sums + a's new mean (4 B 8), every rescanned row's
+                  live D entries (rescans counted by the kernel x mean R x 8);
+          stream: the live regions' mean columns once per step, sum_steps R (8B + 16);
+          w = 0:  ~10 band-sum rows of 8B bytes per step;
+      all-pairs D init (FP64): sum over leaves of R0(R0+1)/2 pairs x (3B + 5) flops,
+        against the measured DFMA flop rate (rhseg_fp64_fma_peak)."""
     import ctypes
 
     from paper_2106_12942_b200 import _lib
 
+    lib = _lib.load()
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     side = 1 << (levels - 1)
     se = edge // side
     nleaf = side * side
     R0 = se * se
-    t = WORKLOADS[name][4]
-    loop_ms, dinit_ms = phases[2], phases[1]
-    if loop_ms >= dinit_ms:
-        # leaves dominate (>99% of steps at t=16); count leaf-level steps only
-        resc = ctypes.c_int64(0)
-        _lib.check(_lib.load().rhseg_result_rescans(ctx.handle, levels, ctypes.byref(resc)), "rescans")
-        apo = w > 0 and MEASURE_OF.get(name) != "sam" and os.environ.get("RHSEG_APO", "1") != "0"
-        if apo:
-            # no mean stream: per step D rows a and b are read and row + column a' written
-            # (4 R 8 bytes), a's and b's band sums and a's new mean (4 B 8), plus every
-            # rescanned row's live D entries (rescans counted by the kernel x mean R)
-            steps = range(t + 1, R0 + 1)
-            per_sec = sum(4 * R * 8 + 4 * bands * 8 for R in steps)
-            rbar = sum(steps) / max(1, len(steps))
-            note = ("APO loop (latency/issue-bound step chain, not a stream): sum_steps (4R*8 + 4B*8) + "
-                    "rescans*mean(R)*8 bytes; %d leaf-level rescans" % resc.value)
-            per_sec += resc.value * rbar * 8 / nleaf
-        elif w > 0:
-            per_sec = sum(R * (8 * bands + 16) for R in range(t + 1, R0 + 1))
-            note = "streams the live regions' fp64 means once per step: sum_steps R_live*(8B+16)"
-        else:  # adjacency only: a's neighbours' band sums (~8 on an 8-connected grid) + a's own
-            per_sec = (R0 - t) * 10 * 8 * bands
-            note = "w=0: ~10 band-sum rows of 8B bytes per step (latency-bound, not a stream)"
-        algo = nleaf * per_sec
-        achieved = algo / (loop_ms * 1e-3) / 1e9
-        return {"kernel": "hseg_loop_kernel (persistent per-section merge loop)", "bound": "hbm",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": ncu_traffic(name, "hseg_loop_kernel"),
-                "algorithmic_bytes": algo, "algorithmic_model": note, "kernel_ms": loop_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
-    fp64 = ctypes.c_double(0.0)
-    _lib.check(_lib.load().rhseg_fp64_peak(ctx.handle, ctypes.byref(fp64)), "fp64_peak")
-    if w > 0:
-        pairs = nleaf * R0 * (R0 + 1) // 2
-        ops = pairs * (3 * bands + 5)
+    t = WORKLOADS[name][4] if levels == 1 else WORKLOADS[name][5]
+    loop_ms, dinit_ms = float(phases[2]), float(phases[1])
+    leaf = leaf or _lib.level_info(handle, levels)
+    var = leaf["variant"]
+    resc_per_sec = leaf["rescans"] / max(1, leaf["nsec"])  # (multi-GPU: from this rank's leaves)
+    steps = range(t + 1, R0 + 1)
+    if var in (2, 3):
+        rbar = sum(steps) / max(1, len(steps))
+        per_sec = sum(4 * R * 8 + 4 * bands * 8 for R in steps) + resc_per_sec * rbar * 8
+        note = ("APO loop: sum_steps (4R*8 + 4B*8) + rescans*mean(R)*8 bytes; %.0f rescans per leaf "
+                "(latency-bound step chain, not a stream)" % resc_per_sec)
+    elif var == 1:
+        per_sec = sum(R * (8 * bands + 16) for R in steps)
+        note = "mean-stream loop: the live regions' fp64 means once per step, sum_steps R_live*(8B+16)"
     else:
-        ops = 0
-    achieved = ops / (dinit_ms * 1e-3) / 1e12
-    peak = fp64.value / 1e12
-    return {"kernel": "dinit_dense_kernel (all-pairs fp64 dissimilarity)", "bound": "fp64",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-            "traffic": ncu_traffic(name, "dinit_dense_kernel"), "kernel_ms": dinit_ms,
-            "peak_source": "measured live by rhseg_fp64_peak (DSUB+DMUL+DADD issue rate); "
-                           "MEASURED_PEAKS.json has no fp64 figure"}
+        per_sec = (R0 - t) * 10 * 8 * bands
+        note = "w=0 loop: ~10 band-sum rows of 8B bytes per step (latency-bound, not a stream)"
+    algo = nleaf * per_sec
+    achieved = algo / (loop_ms * 1e-3) / 1e9 if loop_ms > 0 else 0.0
+    loop = {"kernel": "hseg_apo_kernel (APO merge loop)" if var == 2 else "hseg_loop_kernel (merge loop)",
+            "loop_variant": leaf["loop"], "ctas_per_section": leaf["cluster"],
+            "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": ncu_traffic(name, "hseg_apo_kernel" if var == 2 else "hseg_loop_kernel"),
+            "algorithmic_bytes": algo, "algorithmic_model": note, "kernel_ms": loop_ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
+    fma = ctypes.c_double(0.0)
+    _lib.check(lib.rhseg_fp64_fma_peak(handle, ctypes.byref(fma)), "fp64_fma_peak")
+    flops = nleaf * (R0 * (R0 + 1) // 2) * (3 * bands + 5) if w > 0 else 0
+    ach = flops / (dinit_ms * 1e-3) / 1e12 if dinit_ms > 0 else 0.0
+    peak = fma.value / 1e12
+    dinit = {"kernel": "dinit_dense_kernel (all-pairs fp64 dissimilarity)" if w > 0 else "dinit_sparse_kernel",
+             "bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+             "frac": ach / peak if peak else None, "traffic": ncu_traffic(name, "dinit_dense_kernel"),
+             "kernel_ms": dinit_ms, "algorithmic_flops": flops,
+             "algorithmic_model": "leaf pairs R0(R0+1)/2 x (3B+5) flops (sub, mul, add per band + finish)",
+             "peak_source": "measured live: rhseg_fp64_fma_peak (DFMA loop, 2 flops/instr)"}
+    if loop_ms >= dinit_ms:
+        return loop, dinit
+    return dinit, loop
 
 
 def main(argv=None):

@@ -186,9 +186,23 @@ int rhseg_result_launches(rhseg_ctx *ctx, int64_t *n);
 /* Rows the merge loops of the last run rescanned from D (level <= 0: all levels) --
  * the traffic model of the loop's roofline (bench.py). */
 int rhseg_result_rescans(rhseg_ctx *ctx, int32_t level, int64_t *n);
+/* Which merge loop ran on one level of the last run (the roofline model follows it):
+ * RHSEG_LOOP_ADJACENT (w = 0), RHSEG_LOOP_STREAM (mean-stream loop: SAM, thread-block
+ * clusters, RHSEG_APO=0), RHSEG_LOOP_APO (apo_loop.cu), RHSEG_LOOP_APO_V1 (the first APO
+ * variant, RHSEG_APO_V1=1); plus sections, padded capacity, CTAs per section, merges.
+ * Any output pointer may be NULL. */
+#define RHSEG_LOOP_ADJACENT 0
+#define RHSEG_LOOP_STREAM 1
+#define RHSEG_LOOP_APO 2
+#define RHSEG_LOOP_APO_V1 3
+int rhseg_result_level_info(rhseg_ctx *ctx, int32_t level, int32_t *nsec, int32_t *rp, int32_t *cluster,
+                            int32_t *loop_variant, int64_t *merges);
 /* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure
  * sub/mul/add loop over the whole GPU (roofline denominator). */
 int rhseg_fp64_peak(rhseg_ctx *ctx, double *ops_per_s);
+/* FP64 fused multiply-add probe: achieved fp64 flops/s (2 per DFMA) of a pure DFMA
+ * loop over the whole GPU -- the FP64 flop roofline of the all-pairs D init. */
+int rhseg_fp64_fma_peak(rhseg_ctx *ctx, double *flops_per_s);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,8 @@ def lib():
         L.oracle_rhseg_replay_leaves.restype = i64
         L.oracle_run_leaf.argtypes = [vp, i64, i64, i64, i64, i64, f64, i64, i32, i64]
         L.oracle_run_leaf.restype = i64
+        L.oracle_run_leaves.argtypes = [vp, i64, i64, i64, vp, vp, i64, f64, i64, i32, vp]
+        L.oracle_run_leaves.restype = None
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_set_threads.restype = None
         L.oracle_set_incremental.argtypes = [ctypes.c_int]
@@ -219,3 +221,18 @@ def run_leaf(samples, orow, ocol, sec_edge, weight, target, connectivity=8, max_
     nb, edge, _ = samples.shape
     return lib().oracle_run_leaf(_p(samples), edge, nb, orow, ocol, sec_edge, float(weight),
                                  int(target), int(connectivity), int(max_steps))
+
+
+def run_leaves(samples, origins, sec_edge, weight, target, connectivity=8):
+    """Section-parallel CPU baseline: whole leaves (run_leaf, recursive.py:130-142),
+    one leaf per host thread (the process-per-section strategy of cluster.py), each
+    leaf's scans single-threaded. origins: [(row, col), ...]. Returns merges per leaf."""
+    samples = np.ascontiguousarray(samples, dtype=np.float32)
+    nb, edge, _ = samples.shape
+    o = np.ascontiguousarray(np.asarray(origins, dtype=np.int64).reshape(-1, 2))
+    orow = np.ascontiguousarray(o[:, 0])
+    ocol = np.ascontiguousarray(o[:, 1])
+    merges = np.zeros(len(o), np.int64)
+    lib().oracle_run_leaves(_p(samples), edge, nb, len(o), _p(orow), _p(ocol), int(sec_edge), float(weight),
+                            int(target), int(connectivity), _p(merges))
+    return merges

@@ -85,11 +85,13 @@ _SIGS = {
     "rhseg_result_phase_ms": [vp, vp],
     "rhseg_result_launches": [vp, vp],
     "rhseg_result_rescans": [vp, ctypes.c_int32, vp],
+    "rhseg_result_level_info": [vp, i32, vp, vp, vp, vp, vp],
     "rhseg_format_float": [f64, vp, i32],
     "rhseg_sha256_hex": [vp, i64, vp],
     "rhseg_write_outputs_host": [ctypes.c_char_p, ctypes.c_char_p, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp, vp],
     "rhseg_fp64_peak": [vp, vp],
+    "rhseg_fp64_fma_peak": [vp, vp],
 }
 EXPORTS = tuple(_SIGS)
 
@@ -202,3 +204,30 @@ def make_params(weight, target, section_target, levels, connectivity=8, measure=
     p.measure = int(measure)
     p.cluster = int(cluster)
     return p
+
+
+LOOP_NAMES = {0: "adjacent (w=0)", 1: "mean stream", 2: "APO", 3: "APO v1"}
+
+
+def level_info(handle, level: int) -> dict:
+    """Which merge loop ran on one level of the context's last run, its sections,
+    capacity, CTAs per section, merges and D-row rescans (rhseg_result_level_info /
+    rhseg_result_rescans)."""
+    L = load()
+    ns, rp, cl, var = (ctypes.c_int32(0) for _ in range(4))
+    mg, rs = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(L.rhseg_result_level_info(handle, level, ctypes.byref(ns), ctypes.byref(rp), ctypes.byref(cl),
+                                    ctypes.byref(var), ctypes.byref(mg)), "rhseg_result_level_info")
+    check(L.rhseg_result_rescans(handle, level, ctypes.byref(rs)), "rhseg_result_rescans")
+    return {"nsec": ns.value, "rp": rp.value, "cluster": cl.value, "variant": var.value,
+            "loop": LOOP_NAMES.get(var.value, str(var.value)), "merges": mg.value, "rescans": rs.value}
+
+
+def phase_ms(handle):
+    """Per-kernel device ms of the context's last run: [init, all-pairs D, loops, stitch+labels]."""
+    import numpy as np
+
+    ms = np.zeros(4, np.float32)
+    check(load().rhseg_result_phase_ms(handle, ms.ctypes.data_as(ctypes.c_void_p)), "rhseg_result_phase_ms")
+    return ms.astype(np.float64)
+

@@ -70,6 +70,24 @@ __global__ void fp64_probe_kernel(double* out, int iters) {
     if (s == 12345.0) out[threadIdx.x] = s;  // keep the loop alive
 }
 
+__global__ void fp64_fma_probe_kernel(double* out, int iters) {
+    double x[8], y[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        x[q] = 1.0 + 1e-3 * (threadIdx.x + q);
+        y[q] = 0.0;
+    }
+    const double m = 1.0000001;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) y[q] = __fma_rn(x[q], m, y[q]);  // one DFMA = 2 flops
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += y[q];
+    if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 }  // namespace rhseg
 
 using namespace rhseg;
@@ -473,9 +491,11 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
         const double tot = (double)(ph[0] + ph[1] + ph[2] + ph[3] + ph[4]) + 1e-9;
         fprintf(stderr,
                 "[rhseg profile] level %d: %d sections x C=%d, Rp=%d, %lld steps, %.0f cycles/step (per CTA): "
-                "argmin %.1f%% combine %.1f%% merge %.1f%% row-a %.1f%% rescan %.1f%%, %.2f rescans/step\n",
+                "%s %.1f%% %s %.1f%% %s %.1f%% %s %.1f%% %s %.1f%%, %.2f rescans/step\n",
                 lv.level, lv.nsec, lv.C, lv.Rp, steps, tot / (double)std::max(1LL, steps) / lv.C,
-                100 * ph[0] / tot, 100 * ph[1] / tot, 100 * ph[2] / tot, 100 * ph[3] / tot, 100 * ph[4] / tot,
+                "argmin", 100 * ph[0] / tot, lv.sb.apo ? "rule" : "combine", 100 * ph[1] / tot,
+                lv.sb.apo ? "merge||rescans" : "merge", 100 * ph[2] / tot, lv.sb.apo ? "row-a'+offers" : "row-a",
+                100 * ph[3] / tot, lv.sb.apo ? "publish" : "rescan", 100 * ph[4] / tot,
                 (double)ph[5] / (double)std::max(1LL, steps));
         if (ph[8] + ph[9] + ph[11])
             fprintf(stderr, "[rhseg profile] level %d APO per step: %.2f exact offers, %.2f a-candidates, "
@@ -985,6 +1005,33 @@ int rhseg_result_rescans(rhseg_ctx* c, int32_t level, int64_t* n) {
     return RHSEG_OK;
 }
 
+int rhseg_result_level_info(rhseg_ctx* c, int32_t level, int32_t* nsec, int32_t* rp, int32_t* cluster,
+                            int32_t* loop_variant, int64_t* merges) {
+    if (!c) return fail(RHSEG_E_INVALID, "NULL argument");
+    for (auto& lv : c->levels) {
+        if (lv.imported || lv.level != level) continue;
+        if (nsec) *nsec = lv.nsec;
+        if (rp) *rp = lv.Rp;
+        if (cluster) *cluster = lv.C;
+        if (loop_variant) {
+            static const bool v1 = [] {
+                const char* e = getenv("RHSEG_APO_V1");
+                return e && e[0] == '1';
+            }();
+            *loop_variant = !lv.sb.spec ? RHSEG_LOOP_ADJACENT
+                            : lv.sb.apo ? (v1 ? RHSEG_LOOP_APO_V1 : RHSEG_LOOP_APO)
+                                        : RHSEG_LOOP_STREAM;
+        }
+        if (merges) {
+            long long t = 0;
+            for (int x : lv.nlogh) t += x;
+            *merges = t;
+        }
+        return RHSEG_OK;
+    }
+    return fail(RHSEG_E_INVALID, "level " + std::to_string(level) + " was not run by this context");
+}
+
 int rhseg_result_launches(rhseg_ctx* c, int64_t* n) {
     if (!c || !n) return fail(RHSEG_E_INVALID, "NULL argument");
     *n = c->launches;
@@ -1345,6 +1392,29 @@ int rhseg_fp64_peak(rhseg_ctx* c, double* ops_per_s) {
     cudaEventDestroy(b);
     cudaFree(out);
     *ops_per_s = (double)blocks * threads * iters * 8.0 * 3.0 / (ms * 1e-3);
+    return RHSEG_OK;
+}
+
+int rhseg_fp64_fma_peak(rhseg_ctx* c, double* flops_per_s) {
+    if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
+    CK(cudaSetDevice(c->device));
+    double* out = nullptr;
+    CK(cudaMalloc(&out, 1024 * sizeof(double)));
+    const int blocks = c->nsm * 8, threads = 256, iters = 20000;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp64_fma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, 100);
+    cudaEventRecord(a, c->stream);
+    fp64_fma_probe_kernel<<<blocks, threads, 0, c->stream>>>(out, iters);
+    cudaEventRecord(b, c->stream);
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    *flops_per_s = (double)blocks * threads * iters * 8.0 * 2.0 / (ms * 1e-3);
     return RHSEG_OK;
 }
 

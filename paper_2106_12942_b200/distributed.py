@@ -238,6 +238,8 @@ class ShardedRhseg:
     """torch.distributed (NCCL) sharded RHSEG: call step(cube) on every rank."""
 
     def __init__(self, params, edge: int, bands: int, device: int, connectivity: int = 8):
+        self.record = False  # keep this rank's lower-level phases/loop info (bench)
+        self.last_block = None
         import torch
         import torch.distributed as dist
 
@@ -300,6 +302,10 @@ class ShardedRhseg:
         if self.block is not None:
             self.runner.run_block(cube.data_ptr(), self.top, self.block, stream)
             nsec, rp, _, R0, nlog = self.runner.top_info()
+            if self.record:  # this rank's lower levels (the bench's per-rank roofline)
+                self.torch.cuda.synchronize(self.dev)
+                self.last_block = {"phases": _lib.phase_ms(self.runner.ctx.handle),
+                                   "leaf": _lib.level_info(self.runner.ctx.handle, self.levels)}
         else:
             nsec, rp, R0, nlog = 0, 32, np.zeros(0, np.int32), np.zeros(0, np.int32)
         # metadata exchange: common capacity, per-section sizes
@@ -408,20 +414,21 @@ class ShardedRhseg:
 # ---------------------------------------------------------------------------
 # bench leg (N > 1 under torchrun)
 # ---------------------------------------------------------------------------
-def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, cpu_sample):
+def bench_sharded(args, bm):
+    """N > 1 leg of bench.py (launched by torchrun, one rank per GPU). `bm` is the
+    bench module (workload table, config dict, clock sampler, CPU leg, roofline model);
+    the package never imports the top-level script itself."""
+    import ctypes
     import os
+    import time
 
     import torch
     import torch.distributed as dist
 
     from .recursive import HsegParams, RhsegParams
-
-    import ctypes
-    import time
-
-    from bench import MEASURE_OF
-
     from .synth import gen_synthetic
+
+    WORKLOADS, make_cube, cube_shape, ClockSampler = bm.WORKLOADS, bm.make_cube, bm.cube_shape, bm.ClockSampler
 
     # one process per GPU; RHSEG_DIST_BACKEND=gloo lets several ranks share one GPU
     # (the single-GPU test box) -- collectives then stage through host memory
@@ -455,13 +462,15 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
             cube[:, r0:r1, :].copy_(host[:, :r1 - r0, :], non_blocking=True)
 
     upload()
-    params = RhsegParams(HsegParams(w, t, MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
+    params = RhsegParams(HsegParams(w, t, bm.MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
     sh = ShardedRhseg(params, edge, bands, local)
+    sh.record = True
     flush = torch.empty(2 * 126 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     for _ in range(args.warmup):
         sh.step(cube)
     torch.cuda.synchronize()
     times, launches = [], 0
+    phases = np.zeros(4)
     n = ctypes.c_int64()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -470,13 +479,17 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            sh.step(cube)
+            sh.step(cube, gather_logs=False)  # (the log gather is part of the e2e leg below)
             e1.record()
             torch.cuda.synchronize()
             dist.barrier()
             times.append(e0.elapsed_time(e1))
             sh.runner.lib.rhseg_result_launches(sh.runner.ctx.handle, ctypes.byref(n))
             launches += int(n.value)
+            if sh.block is not None:
+                phases += sh.last_block["phases"]
+    phases /= max(1, args.steps)
+    sh.record = False
     # end to end: this rank's rows H2D, the sharded run, logs gathered to rank 0,
     # root labels D2H on rank 0 (wall clock, max over ranks)
     lab = np.empty(edge * edge, np.int32)
@@ -495,28 +508,43 @@ def bench_sharded(args, WORKLOADS, DESCR, make_cube, cube_shape, ClockSampler, c
         torch.cuda.synchronize()
         e2e.append(time.perf_counter() - t0)
         del parts
-    vals = torch.tensor([float(np.mean(times)), float(np.median(e2e)) * 1e3, float(launches)], device=dev)
+    vals = torch.tensor([float(np.mean(times)), float(np.median(e2e)) * 1e3, float(launches), *phases.tolist()],
+                        device=dev)
     mx = vals.clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(vals, op=dist.ReduceOp.SUM)
     ms, e2e_ms, launches_total = float(mx[0]), float(mx[1]), int(vals[2].item())
+    ph_max = mx[3:7].cpu().numpy()  # per-kernel device ms of the slowest rank
     if rank == 0:
         npxb = edge * edge * bands
+        leaf = sh.last_block["leaf"] if sh.block is not None else None
+        roof = roof2 = None
+        if leaf is not None:
+            # the slowest rank's loop time against the whole job's algorithmic work
+            roof, roof2 = bm.roofline(name, edge, bands, levels, w, ph_max, sh.runner.ctx.handle, leaf=leaf)
         line = {
             "metric": "RHSEG pixel-bands/sec", "value": npxb / (ms * 1e-3), "unit": "pixel-bands/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen_synthetic, bit-identical to the reference generator)",
-            "config": {"workload": DESCR[name], "edge": edge, "bands": bands, "levels": levels,
-                       "parallelism": f"subtree sharding: level-{top} subtrees over {world} ranks, NCCL gather to rank 0",
-                       "l2": "flushed between timed steps (2x126 MB write)"},
+            "config": bm.config_of(name),
+            "execution": f"subtree sharding: level-{top} subtrees over {world} ranks (no data-path collective "
+                         f"below level {top}), NCCL gather of the level-{top} section states to rank 0, which "
+                         f"runs the levels above",
+            "phase_ms_max_over_ranks": {"init_stitch": float(ph_max[0]), "dinit_allpairs": float(ph_max[1]),
+                                        "merge_loop": float(ph_max[2]), "resolve_labels": float(ph_max[3])},
             "gpu_launches": launches_total,
+            "roofline": roof,
+            "roofline_secondary": roof2,
             "e2e": {"value": npxb / (e2e_ms * 1e-3), "unit": "pixel-bands/s",
                     "h2d_bytes_per_step": npxb * 4, "d2h_bytes_per_step": edge * edge * 4,
                     "ms_per_step": e2e_ms,
                     "note": "each rank uploads its own rows; merge logs gathered to rank 0 over NCCL"},
             "clocks": clk.summary(),
         }
+        if not getattr(args, "no_cpu_baseline", False):
+            cb = bm.cpu_sample(name, make_cube(name), seconds_hint=args.ref_seconds)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()
