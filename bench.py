@@ -462,10 +462,12 @@ def roofline(name, edge, bands, levels, w, phases, handle, leaf=None):
         note = "w=0 loop: ~10 band-sum rows of 8B bytes per step (latency-bound, not a stream)"
     algo = nleaf * per_sec
     achieved = algo / (loop_ms * 1e-3) / 1e9 if loop_ms > 0 else 0.0
-    loop = {"kernel": "hseg_apo_kernel (APO merge loop)" if var == 2 else "hseg_loop_kernel (merge loop)",
+    kname = {3: "hseg_apo_kernel", 0: "hseg_adj_kernel"}.get(var, "hseg_loop_kernel") if leaf["cluster"] == 1 \
+        else "hseg_loop_kernel"
+    loop = {"kernel": kname + " (persistent per-section merge loop)",
             "loop_variant": leaf["loop"], "ctas_per_section": leaf["cluster"],
             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic(name, "hseg_apo_kernel" if var == 2 else "hseg_loop_kernel"),
+            "traffic": ncu_traffic(name, kname),
             "algorithmic_bytes": algo, "algorithmic_model": note, "kernel_ms": loop_ms,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"}
     fma = ctypes.c_double(0.0)

@@ -188,13 +188,13 @@ int rhseg_result_launches(rhseg_ctx *ctx, int64_t *n);
 int rhseg_result_rescans(rhseg_ctx *ctx, int32_t level, int64_t *n);
 /* Which merge loop ran on one level of the last run (the roofline model follows it):
  * RHSEG_LOOP_ADJACENT (w = 0), RHSEG_LOOP_STREAM (mean-stream loop: SAM, thread-block
- * clusters, RHSEG_APO=0), RHSEG_LOOP_APO (apo_loop.cu), RHSEG_LOOP_APO_V1 (the first APO
- * variant, RHSEG_APO_V1=1); plus sections, padded capacity, CTAs per section, merges.
+ * clusters, RHSEG_APO=0), RHSEG_LOOP_APO (the APO loop, hseg_kernels.cu), RHSEG_LOOP_APO_RECUT
+ * (apo_loop.cu, RHSEG_APO_V2=1); plus sections, padded capacity, CTAs per section, merges.
  * Any output pointer may be NULL. */
 #define RHSEG_LOOP_ADJACENT 0
 #define RHSEG_LOOP_STREAM 1
 #define RHSEG_LOOP_APO 2
-#define RHSEG_LOOP_APO_V1 3
+#define RHSEG_LOOP_APO_RECUT 3
 int rhseg_result_level_info(rhseg_ctx *ctx, int32_t level, int32_t *nsec, int32_t *rp, int32_t *cluster,
                             int32_t *loop_variant, int64_t *merges);
 /* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure

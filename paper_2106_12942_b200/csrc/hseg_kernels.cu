@@ -30,49 +30,16 @@
 // the log's values after the loop. Same merge sequence, far fewer bytes per step.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <type_traits>
 
 #include "rhseg_batch.h"
 #include "rhseg_device.cuh"
+#include "apo_device.cuh"
 
 namespace rhseg {
 
-// D entries: an exact value is a non-negative double (sign bit clear); an interval
-// (APO sections only, see the APO section below) is [sign=1 | centre c with its low 6
-// mantissa bits replaced by k] = c (1 -/+ 2^(k-46)).
-constexpr double kU64 = 1.1102230246251565e-16;
-constexpr int kApoKMax = 45;  // widest encodable interval: c (1 -/+ 1/2)
-__device__ __forceinline__ bool d_is_interval(double v) { return __double_as_longlong(v) < 0; }
-__device__ __forceinline__ void d_decode(double c, int k, double& lo, double& hi) {
-    const double rho = __longlong_as_double((long long)(k - 46 + 1023) << 52);
-    lo = __dmul_rd(c, 1.0 - rho);  // 1 -/+ rho are exact for 2^-46 <= rho <= 1/2
-    hi = __dmul_ru(c, 1.0 + rho);
-}
-__device__ __forceinline__ void d_unpack(double v, double& lo, double& hi) {
-    const long long b = __double_as_longlong(v);
-    if (b < 0) d_decode(__longlong_as_double(b & 0x7fffffffffffffc0LL), (int)(b & 63), lo, hi);
-    else lo = hi = v;
-}
-// encode [lo, hi] (0 < lo <= hi < inf); false when the interval is too wide to encode
-__device__ __forceinline__ bool d_pack_interval(double lo, double hi, double& out) {
-    if (lo == hi) { out = lo; return true; }
-    if (!(lo > 0.0) || !(hi < kInf)) return false;
-    const long long cb = __double_as_longlong(0.5 * lo + 0.5 * hi) & 0x7fffffffffffffc0LL;
-    const double c = __longlong_as_double(cb);  // truncated centre
-    // first guess from the exponents of the half-width and the centre, then verify
-    // with the decoder itself (rarely more than one extra iteration)
-    const double w = fmax(hi - c, c - lo);
-    const int ew = (int)((__double_as_longlong(w) >> 52) & 0x7ff), ec = (int)((cb >> 52) & 0x7ff);
-    int k = max(0, ew - ec + 47);
-    for (; k <= kApoKMax; ++k) {
-        double l2, h2;
-        d_decode(c, k, l2, h2);
-        if (l2 <= lo && h2 >= hi) break;
-    }
-    if (k > kApoKMax) return false;
-    out = __longlong_as_double((long long)(0x8000000000000000ULL | (unsigned long long)cb | (unsigned long long)k));
-    return true;
-}
 #ifndef RHSEG_DINIT_FMA
 #define RHSEG_DINIT_FMA 1  // APO sections: fused-multiply-add all-pairs init into intervals
 #endif
@@ -110,11 +77,11 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     const uint32_t* __restrict__ cnt = bt.count + (size_t)sec * Rp;
     const double* __restrict__ n2 = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
 
-    // band staging (sA, sB) and the transpose tile (sT) share one buffer: sT is
-    // only touched after the last band chunk's trailing __syncthreads().
-    __shared__ __align__(16) double smraw[kTile * (kTile + 1)];
-    double (*sA)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw);
-    double (*sB)[kTile] = reinterpret_cast<double (*)[kTile]>(smraw + kKB * kTile);
+    // band staging: two buffers of (sA, sB) chunks filled by cp.async while the other
+    // is consumed (double buffering); the transpose tile sT aliases the staging area
+    // and is only touched after the last chunk's trailing __syncthreads()
+    constexpr int kStage = 2 * kKB * kTile;  // doubles per buffer (A then B)
+    __shared__ __align__(16) double smraw[(2 * kStage > kTile * (kTile + 1)) ? 2 * kStage : kTile * (kTile + 1)];
     double (*sT)[kTile + 1] = reinterpret_cast<double (*)[kTile + 1]>(smraw);
     // thread (tx, ty) owns rows i0 + 4 ty + p and columns j0 + 4 tx + q: both operand
     // quads are contiguous in shared memory (two 16-byte loads each)
@@ -125,17 +92,33 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
 #pragma unroll
         for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
 
-    for (int k0 = 0; k0 < B; k0 += kKB) {
-        const int kn = min(kKB, B - k0);
-        for (int e = threadIdx.x; e < kKB * kTile; e += kThreads) {
-            const int kk = e / kTile, r = e % kTile;
-            const bool in = kk < kn;
-            sA[kk][r] = in ? mu[(size_t)(k0 + kk) * Rp + i0 + r] : 0.0;
-            sB[kk][r] = in ? mu[(size_t)(k0 + kk) * Rp + j0 + r] : 0.0;
+    // one chunk = kKB bands x 64 rows of each operand = 2 x kKB x 32 16-byte pieces;
+    // bands past B are zero-filled (src-size 0): +0.0 to every accumulator, an identity
+    auto stage = [&](int k0, int buf) {
+        double* dst = smraw + buf * kStage;
+        for (int e = threadIdx.x; e < 2 * kKB * (kTile / 2); e += kThreads) {
+            const int op = e / (kKB * (kTile / 2)), r = e % (kKB * (kTile / 2));
+            const int kk = r / (kTile / 2), c = r % (kTile / 2);
+            const int k = k0 + kk;
+            const double* src = mu + (size_t)min(k, B - 1) * Rp + (op ? j0 : i0) + 2 * c;
+            const uint32_t d = smem_u32(dst + op * kKB * kTile + kk * kTile + 2 * c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(k < B ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int nchunk = (B + kKB - 1) / kKB;
+    stage(0, 0);
+    for (int ch = 0; ch < nchunk; ++ch) {
+        if (ch + 1 < nchunk) {
+            stage((ch + 1) * kKB, (ch + 1) & 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
         __syncthreads();
-        // always kKB bands: the zero padding of a short last chunk adds exactly +0.0
-        // to every accumulator (never -0.0), an identity, so the bits are unchanged
+        const double (*sA)[kTile] = reinterpret_cast<const double (*)[kTile]>(smraw + (ch & 1) * kStage);
+        const double (*sB)[kTile] = reinterpret_cast<const double (*)[kTile]>(smraw + (ch & 1) * kStage + kKB * kTile);
 #pragma unroll
         for (int kk = 0; kk < kKB; ++kk) {
             const double2 a01 = *reinterpret_cast<const double2*>(&sA[kk][4 * ty]);
@@ -156,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
                     }
                 }
         }
-        __syncthreads();
+        __syncthreads();  // buffer ch & 1 is refilled by the next iteration's stage()
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -410,122 +393,6 @@ struct Top2Lists {
     uint8_t* cx;
 };
 
-// ---- APO: row a' without the mean stream (w > 0, BSMSE/Euclidean, one CTA per section)
-// After merging b into a, the new mean is m' = lam m_a + (1 - lam) m_b + e (lam = n_a/n,
-// e = the rounding of the new sums / count), and for every region j the parallelogram
-// identity gives, exactly in real arithmetic,
-//     || lam m_a + (1-lam) m_b - m_j ||^2 = lam T_aj + (1-lam) T_bj - lam (1-lam) T_ab
-// with T_xy = ||m_x - m_y||^2. D already holds d(a, j), d(b, j) and d(a, b), and the
-// reference value satisfies d^2 = C T (1 + eps) with |eps| <= E = (B + 8) u (C = n_x n_y /
-// (n_x + n_y) for BSMSE, 1 for Euclidean: ascending-band sum of B rounded squares, the
-// coefficient product, sqrt). So two D rows (16 bytes per column instead of the 8B + 16
-// bytes of a mean column) give a rigorous interval around the reference's d(a', j):
-// directed-rounding arithmetic throughout, ||e|| <= 3.01 u max ||m|| (max over the
-// section's initial means, which bound every later mean). Entries the interval cannot
-// settle are evaluated exactly (warp_exact) -- offers that may beat a row's cached best
-// (0.3 per step on a C4 leaf), a's best when several columns tie within their intervals,
-// argmin winners, multi-candidate rescans -- so every dissimilarity the merge sequence
-// and the log see is the reference's exact fp64 value.
-//
-// D entries: an exact value is a non-negative double (sign bit clear). An interval is
-// [sign=1 | centre c with its low 6 mantissa bits replaced by k] = c (1 -/+ 2^(k-46)),
-// decoded with directed multiplies (single DMUL.RM/.RP instructions).
-//
-// The interval arithmetic itself is round-to-nearest with explicit slack (directed
-// division/sqrt are long software sequences): with u = 2^-53, every quantity below is
-// within a few u of its real value, and each bound is widened by at least twice the
-// worst-case accumulated error:
-//   A = d(a,j)^2 (1/n_a + 1/n_j) = T_aj (1 + eps) (1 +- 5u)        (d^2 = C T (1 + eps))
-//   V = lam A + (1-lam) B - lam(1-lam) T_ab,  |V - V_true| <= (E + 12u) S,  S = sum of |terms|
-//   ||v|| in [sqrt(V_lo - 2(E+16u)S), sqrt(V_hi + 2(E+16u)S)]   (the rounding of the
-//        subtraction and sqrt is covered by the doubled slack; ||v|| <= 2 max||m||)
-//   sqrt(T') in [||v|| -+ ee], ee = 10u max||m|| (>= 3.02u max||m|| for e, + sqrt/sub rounding)
-//   d(a',j) = sqrt(C') sqrt(T') sqrt(1 + eps'),  widened by 2 (E/2 + 8u) relative.
-// Per-step constants of the row-a' pass (identical in every thread).
-struct ApoStep {
-    double lam, mu, kt_lo, kt_hi;  // na/nn, nb/nn, lam mu T_ab (d(a, b) may be an interval)
-    double rna, rnb, rnn;
-    double vslack, ee, mrel;
-};
-template <int M>
-__device__ __forceinline__ ApoStep apo_step(double na, double nb, double dab, double E, double ee) {
-    ApoStep p;
-    const double nn = na + nb;
-    p.lam = na / nn;
-    p.mu = nb / nn;
-    p.rna = M == kBsmse ? 1.0 / na : 0.0;
-    p.rnb = M == kBsmse ? 1.0 / nb : 0.0;
-    p.rnn = M == kBsmse ? 1.0 / nn : 0.0;
-    double dl, dh;
-    d_unpack(dab, dl, dh);
-    const double cab = M == kBsmse ? p.rna + p.rnb : 1.0;
-    p.kt_lo = p.lam * p.mu * (dl * dl * cab);
-    p.kt_hi = p.lam * p.mu * (dh * dh * cab);
-    p.vslack = 2.0 * (E + 16.0 * kU64);
-    p.ee = ee;
-    p.mrel = 2.0 * (0.5 * E + 8.0 * kU64);
-    return p;
-}
-// interval around the reference's d(a', j) from the raw D entries d(a, j), d(b, j)
-template <int M>
-__device__ __forceinline__ void apo_interval(const ApoStep& p, double rA, double rB, double nj, double& dlo,
-                                             double& dhi) {
-    double al, ah, bl, bh;
-    d_unpack(rA, al, ah);
-    d_unpack(rB, bl, bh);
-    const double rj = M == kBsmse ? 1.0 / nj : 0.0;
-    const double ca = M == kBsmse ? p.rna + rj : 1.0, cb = M == kBsmse ? p.rnb + rj : 1.0;
-    const double Al = al * al * ca, Ah = ah * ah * ca, Bl = bl * bl * cb, Bh = bh * bh * cb;
-    const double Vl = p.lam * Al + p.mu * Bl - p.kt_hi;
-    const double Vh = p.lam * Ah + p.mu * Bh - p.kt_lo;
-    const double dv = p.vslack * (p.lam * Ah + p.mu * Bh + p.kt_hi);
-    const double nlo = fmax(0.0, sqrt(fmax(0.0, Vl - dv)) - p.ee);
-    const double nhi = sqrt(fmax(0.0, Vh + dv)) + p.ee;
-    const double sc = M == kBsmse ? sqrt(1.0 / (p.rnn + rj)) : 1.0;  // sqrt(C')
-    dlo = nlo * sc * (1.0 - p.mrel);
-    dhi = nhi * sc * (1.0 + p.mrel);
-}
-
-// Exact d(i, j) by one warp (all lanes return it) from two fp64 mean vectors
-// (shared or global memory; APO keeps a region-major copy of the exact cached means):
-// every lane loads its bands up front, the per-band terms are independent, and only
-// the ascending-band sum is a serial chain, fed by shuffles issued ahead of it.
-template <int M>
-__device__ __noinline__ double warp_exact(const double* mi, const double* mj, double ci, double cj, int B,
-                                             int lane) {
-    double s = 0.0;
-    for (int k0 = 0; k0 < B; k0 += 256) {
-        double term[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int k = k0 + 32 * u + lane;
-            const double vi = k < B ? mi[k] : 0.0, vj = k < B ? __ldcg(mj + k) : 0.0;
-            if (M == kSam) {
-                term[u] = __dmul_rn(vi, vj);
-            } else {
-                const double t = __dsub_rn(vi, vj);
-                term[u] = __dmul_rn(t, t);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int kn = min(32, B - (k0 + 32 * u));
-            if (kn <= 0) break;
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) {
-                const double tk = __shfl_sync(0xffffffffu, term[u], kk);
-                if (kk < kn) s = __dadd_rn(s, tk);
-            }
-        }
-    }
-    return pair_finish<M>(ci, cj, s, 0.0, 0.0);
-}
-
-// APO: a's best when its single candidate may be an interval (nothing to compare)
-__device__ __forceinline__ void rb_offer_iv(RowBest& b, double v, int j) {
-    if (__double_as_longlong(v) < 0) { b.d = v; b.j = j; }
-    else rb_offer(b, v, j);
-}
 
 // Epilogue for one column j of the row-a pass: D row/column update, offer
 // (d, a) to row j's caches, mark rows whose cached partner died.
@@ -1933,6 +1800,19 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
 
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
     if (nrun == 0) return 0;
+    // APO sections: the APO variant below; RHSEG_APO_V2=1 selects the re-cut loop of
+    // apo_loop.cu (bit-identical, currently slower: see profiles/r02_apo_v2.md)
+    static const bool v1 = [] {
+        const char* e = getenv("RHSEG_APO_V2");  // the re-cut loop is opt-in while it is slower
+        return !(e && e[0] == '1');
+    }();
+    if (b.apo && !v1) return launch_apo_loop(b, nrun, st);
+    // w = 0, one CTA per section: adj_loop.cu (RHSEG_ADJ_V1=1: the generic loop below)
+    static const bool adj_v1 = [] {
+        const char* e = getenv("RHSEG_ADJ_V1");
+        return e && e[0] == '1';
+    }();
+    if (!b.spec && b.C == 1 && !adj_v1) return launch_adj_loop(b, nrun, st);
     const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure, b.stage_bytes, b.nstages);
     void (*kern)(SectionBatch);
 #define RHSEG_PICK(M)                                                                              \

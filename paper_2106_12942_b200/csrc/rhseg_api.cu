@@ -295,7 +295,10 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     o = 0;
     const size_t oAdj = take(ns * C * Rp * W * 4);
     lv.work_zero = o;
-    const size_t oMu = take(ns * B * Rp * 8), oMu2 = take(spec ? (apo ? 2 : 1) * ns * B * Rp * 8 : 0),  // APO: versioned means
+    // w = 0 (adj_loop.cu, one CTA per section) keeps region-major means in mu2
+    const bool adjl = !spec && lv.C == 1;
+    const size_t oMu = take(ns * B * Rp * 8),
+                 oMu2 = take(spec ? (apo ? 2 : 1) * ns * B * Rp * 8 : (adjl ? ns * B * Rp * 8 : 0)),  // APO: versioned means
                  oRec = take(apo ? ns * Rp * 16 : 0),
                  oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
@@ -347,7 +350,7 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.nresc = reinterpret_cast<long long*>(K + oRs);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
-    b.mu2 = spec ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.mu2 = (spec || adjl) ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
     b.apo_rec = apo ? reinterpret_cast<uint4*>(Wk + oRec) : nullptr;
     b.sums = reinterpret_cast<double*>(Wk + oSums);
     lv.map = reinterpret_cast<int*>(K + oMap);
@@ -1014,12 +1017,12 @@ int rhseg_result_level_info(rhseg_ctx* c, int32_t level, int32_t* nsec, int32_t*
         if (rp) *rp = lv.Rp;
         if (cluster) *cluster = lv.C;
         if (loop_variant) {
-            static const bool v1 = [] {
-                const char* e = getenv("RHSEG_APO_V1");
+            static const bool recut = [] {
+                const char* e = getenv("RHSEG_APO_V2");
                 return e && e[0] == '1';
             }();
             *loop_variant = !lv.sb.spec ? RHSEG_LOOP_ADJACENT
-                            : lv.sb.apo ? (v1 ? RHSEG_LOOP_APO_V1 : RHSEG_LOOP_APO)
+                            : lv.sb.apo ? (recut ? RHSEG_LOOP_APO_RECUT : RHSEG_LOOP_APO)
                                         : RHSEG_LOOP_STREAM;
         }
         if (merges) {
