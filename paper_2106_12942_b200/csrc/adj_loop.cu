@@ -15,55 +15,68 @@
 //      re-point, a' neighbour list); the other warps -- and the merge warps once done --
 //      claim listed rows and re-minimise them over their adjacency from D, excluding a
 //      and b (a rescan reads nothing the merge writes but bits a, b it skips).
-//  (R) row a': one warp per neighbour j of a' forms d(a', j) from the region-major
-//      means (a coalesced 8B-byte row, no division: the mean cache of Appendix A.3,
-//      sums / count, kept per region) with the reference's ascending-band order,
-//      writes D, offers (d, a') to row j; a's best is one block reduction.
+//  (R) row a': d(a', j) for every neighbour j from the region-major means (no division:
+//      the mean cache of Appendix A.3, sums / count, kept per region): a warp loads up to
+//      8 neighbours' rows at once and stages the per-band terms, one lane per neighbour
+//      runs the reference's ascending-band sum; D written, (d, a') offered to row j,
+//      a's best by one block reduction.
 //  (E) one thread publishes the merge (counts, log, a's cache); a's mean row updated.
 // Five block barriers per step (round 1's generic loop: ~12 and a division per band
 // per neighbour, 24k cycles per step on a C5 leaf).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "rhseg_batch.h"
 #include "rhseg_device.cuh"
 
 namespace rhseg {
 
-#ifndef RHSEG_ADJ_MERGE_WARPS
-#define RHSEG_ADJ_MERGE_WARPS 2
-#endif
-#ifndef RHSEG_ADJ_MINBLOCKS
-#define RHSEG_ADJ_MINBLOCKS 3
-#endif
-constexpr int kAdjMergeThreads = RHSEG_ADJ_MERGE_WARPS * 32;
+// CTA shapes: 256 threads (8 warps, two of them merging) for levels with few
+// sections, 128 threads (4 warps, one merging) with up to 7 CTAs per SM when the level
+// has many: the step is a latency chain, so resident sections, not threads per
+// section, set the throughput (C5 leaves: 1024 sections in one wave instead of three).
+template <int NT>
+struct AdjShape {
+    static constexpr int kW = NT / 32;
+    static constexpr int kMergeWarps = NT >= 256 ? 2 : 1;
+    static constexpr int kMergeThreads = kMergeWarps * 32;
+    static constexpr int kMinBlocks = NT >= 256 ? 3 : 7;
+};
 constexpr int kAdjNbList = 512;
+constexpr int kAdjStage = 256;   // doubles of per-warp term staging (row a' pass; the
+                                 // 128-thread shape keeps 7 CTAs per SM within 32 KB)
+constexpr int kAdjStageNb = 8;   // neighbours per warp round
 
 struct AdjSmem {
-    size_t misc, red, cnt, bAd, bAj, inv, nbr, nbl, mua, total;
+    size_t misc, red, cnt, bAd, bAj, inv, nbr, nbl, mua, terms, total;
 };
 __host__ __device__ inline size_t adj_align(size_t x) { return (x + 15) & ~size_t(15); }
-__host__ __device__ inline AdjSmem adj_smem_layout(int Rp, int B) {
+__host__ __device__ inline AdjSmem adj_smem_layout(int Rp, int B, int nwarps) {
     AdjSmem L;
     const size_t R = (size_t)Rp;
     size_t o = 0;
     L.misc = o; o += 128;
-    L.red = o;  o += 2 * kWarps * sizeof(Pair);
+    L.red = o;  o += 2 * 8 * sizeof(Pair);  // [parity][warp] (<= 8 warps)
     L.cnt = o;  o = adj_align(o + R * 4);
     L.bAd = o;  o = adj_align(o + R * 8);
     L.bAj = o;  o = adj_align(o + R * 4);
-    L.inv = o;  o = adj_align(o + R * 4);            // listed rows
+    L.inv = o;  o = adj_align(o + R * 2);            // listed rows
     L.nbr = o;  o = adj_align(o + R * 2);            // neighbours of a'
     L.nbl = o;  o = adj_align(o + kAdjNbList * 2);   // b's neighbours (re-point)
     L.mua = o;  o = adj_align(o + (size_t)B * 8);
+    L.terms = o; o = adj_align(o + (size_t)nwarps * kAdjStage * 8);  // [warp][kAdjStage]
     L.total = o;
     return L;
 }
-size_t adj_loop_smem(int Rp, int B) { return adj_smem_layout(Rp, B).total; }
+size_t adj_loop_smem(int Rp, int B, int nwarps) { return adj_smem_layout(Rp, B, nwarps).total; }
 
 enum { kAmNinv = 0, kAmIctr, kAmNnb, kAmNnbr };
 
+template <int MT>
 __device__ __forceinline__ void adj_bar_merge() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kAdjMergeThreads) : "memory");
+    if (MT == 32) __syncwarp();
+    else asm volatile("bar.sync 1, %0;" ::"n"(MT) : "memory");
 }
 __device__ __forceinline__ unsigned pair_key(int i, int j) {
     return ((unsigned)min(i, j) << 16) | (unsigned)max(i, j);
@@ -73,8 +86,9 @@ __device__ __forceinline__ void dk_offer(double& d, unsigned& k, double d2, unsi
     if (d2 < d || (d2 == d && k2 < k)) { d = d2; k = k2; }
 }
 
-template <int M>
-__global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel(SectionBatch bt) {
+template <int M, int NT>
+__global__ void __launch_bounds__(NT, AdjShape<NT>::kMinBlocks) hseg_adj_kernel(SectionBatch bt) {
+    constexpr int kThreads = NT, kWarps = AdjShape<NT>::kW, kAdjMergeThreads = AdjShape<NT>::kMergeThreads;
     extern __shared__ __align__(128) unsigned char smem[];
     const long long t_entry = clock64();
     const int sec = bt.sec0 + (int)blockIdx.x;
@@ -82,16 +96,17 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
     const int R0 = bt.R0[sec];
     const int B = bt.B, Rp = bt.Rp, W = bt.W;
     const int target = bt.target[sec];
-    const AdjSmem L = adj_smem_layout(Rp, B);
+    const AdjSmem L = adj_smem_layout(Rp, B, kWarps);
     int* misc = reinterpret_cast<int*>(smem + L.misc);
     Pair* red = reinterpret_cast<Pair*>(smem + L.red);
     uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + L.cnt);
     double* bAd = reinterpret_cast<double*>(smem + L.bAd);
     int* bAj = reinterpret_cast<int*>(smem + L.bAj);
-    int* inv = reinterpret_cast<int*>(smem + L.inv);
+    unsigned short* inv = reinterpret_cast<unsigned short*>(smem + L.inv);
     unsigned short* nbr = reinterpret_cast<unsigned short*>(smem + L.nbr);
     unsigned short* nbl = reinterpret_cast<unsigned short*>(smem + L.nbl);
     double* mua = reinterpret_cast<double*>(smem + L.mua);
+    double* terms = reinterpret_cast<double*>(smem + L.terms);
     double* n2s = reinterpret_cast<double*>(misc + 8);  // SAM: squared norm of a's new mean
 
     double* const mr = bt.mu2 + sec * bt.mu_stride();  // region-major exact means [Rp][B]
@@ -156,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
         if (cnt[i] != 0u) mr[e] = __ddiv_rn(sums[e], (double)cnt[i]);  // == the cached mean, bit for bit
     }
     for (int i = tid; i < R0; i += kThreads)
-        if (cnt[i] != 0u) inv[atomicAdd(&misc[kAmNinv], 1)] = i;
+        if (cnt[i] != 0u) inv[atomicAdd(&misc[kAmNinv], 1)] = (unsigned short)i;
     __syncthreads();
     rescan_rows(misc[kAmNinv], -1, -1, [] {}, 0);
     if (tid == 0) { misc[kAmNinv] = 0; misc[kAmIctr] = 0; }
@@ -190,12 +205,18 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
         Pair* scr = red + par * kWarps;
         if (lane == 0) scr[warp] = Pair{gd, (int)(gk >> 16), (int)(gk & 0xffffu)};
         __syncthreads();
-        gd = kInf;
-        gk = 0xffffffffu;
+        {   // every warp combines the kWarps partials in its lanes (3 shuffle rounds)
+            const Pair p = lane < kWarps ? scr[lane] : Pair{kInf, 0, 0};
+            gd = p.d;
+            gk = p.d < kInf ? ((unsigned)p.lo << 16) | (unsigned)p.hi : 0xffffffffu;
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const Pair p = scr[w];
-            if (p.d < kInf) dk_offer(gd, gk, p.d, ((unsigned)p.lo << 16) | (unsigned)p.hi);
+            for (int o = kWarps / 2; o > 0; o >>= 1) {  // (lanes < kWarps hold the partials)
+                const double od = __shfl_xor_sync(0xffffffffu, gd, o);
+                const unsigned ok = __shfl_xor_sync(0xffffffffu, gk, o);
+                dk_offer(gd, gk, od, ok);
+            }
+            gd = __shfl_sync(0xffffffffu, gd, 0);
+            gk = __shfl_sync(0xffffffffu, gk, 0);
         }
         if (!(gd < kInf)) { conv = 1; break; }
         const int a = (int)(gk >> 16), b = (int)(gk & 0xffffu);
@@ -206,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
         // ---- (C) rows whose cached neighbour is a or b ----
         for (int i = tid; i < R0; i += kThreads) {
             if (cnt[i] == 0u || i == a || i == b) continue;
-            if (bAj[i] == a || bAj[i] == b) inv[atomicAdd(&misc[kAmNinv], 1)] = i;
+            if (bAj[i] == a || bAj[i] == b) inv[atomicAdd(&misc[kAmNinv], 1)] = (unsigned short)i;
         }
         __syncthreads();
         const int ni = misc[kAmNinv];
@@ -254,12 +275,12 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
                     else repoint(n);
                 }
             }
-            adj_bar_merge();
+            adj_bar_merge<kAdjMergeThreads>();
             if (M == kSam && tid == 0) *n2s = norm2_seq(mua, 1, B);  // sequential (oracle order)
             const int nb = min(misc[kAmNnb], kAdjNbList);
             for (int k = tid; k < nb; k += kAdjMergeThreads) repoint(nbl[k]);
         };
-        rescan_rows(ni, a, b, merge, RHSEG_ADJ_MERGE_WARPS);
+        rescan_rows(ni, a, b, merge, AdjShape<NT>::kMergeWarps);
         mark(2);
 
         // ---- (R) row a': d(a', j) for every neighbour j, offers, a's best ----
@@ -267,34 +288,54 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
         const double n2a = M == kSam ? *n2s : 0.0;
         double pd = kInf;
         unsigned pj = 0xffffffffu;
-        for (int t = warp; t < nnbr; t += kWarps) {
-            const int j = nbr[t];
-            if (cnt[j] == 0u) continue;  // (never: a' neighbours are live)
-            const double* mj = mr + (size_t)j * B;
-            double s = 0.0;
-            for (int k0 = 0; k0 < B; k0 += 32) {
-                const int k = k0 + lane;
-                const double v = k < B ? __ldcg(mj + k) : 0.0;
-                double term;
-                if (M == kSam) term = __dmul_rn(mua[k < B ? k : 0], v);
-                else {
-                    const double df = __dsub_rn(mua[k < B ? k : 0], v);
-                    term = __dmul_rn(df, df);
-                }
-                const int kn = min(32, B - k0);
+        // per warp, rounds of up to NQ neighbours: the lanes load the neighbours' mean rows
+        // (all loads of a round in flight together) and stage the per-band terms in
+        // shared memory; then one lane per neighbour runs the ascending-band sum -- a
+        // serial chain anyway (a warp-wide shuffle chain would execute it 32 times over)
+        const int NQ = max(1, min(kAdjStageNb, kAdjStage / max(B, 1)));
+        const int KC = kAdjStage / NQ;  // bands staged per pass (all of them unless B > kAdjStage)
+        double* stg = terms + (size_t)warp * kAdjStage;
+        for (int t0 = warp * NQ; t0 < nnbr; t0 += kWarps * NQ) {
+            const int nq = min(NQ, nnbr - t0);
+            double s = 0.0;  // lane q < nq: running ascending-band sum of neighbour t0 + q
+            for (int kc0 = 0; kc0 < B; kc0 += KC) {
+                const int kc1 = min(B, kc0 + KC);
+                for (int k0 = kc0; k0 < kc1; k0 += 32) {
+                    const int k = k0 + lane;
+                    const bool in = k < kc1;
+                    const double m = in ? mua[k] : 0.0;
+                    double v[kAdjStageNb];
 #pragma unroll
-                for (int kk = 0; kk < 32; ++kk) {
-                    const double tk = __shfl_sync(0xffffffffu, term, kk);
-                    if (kk < kn) s = __dadd_rn(s, tk);
+                    for (int q = 0; q < kAdjStageNb; ++q)
+                        v[q] = (q < nq && in) ? __ldcg(mr + (size_t)nbr[t0 + q] * B + k) : 0.0;
+#pragma unroll
+                    for (int q = 0; q < kAdjStageNb; ++q) {
+                        if (q < nq && in) {
+                            double term;
+                            if (M == kSam) term = __dmul_rn(m, v[q]);
+                            else {
+                                const double df = __dsub_rn(m, v[q]);
+                                term = __dmul_rn(df, df);
+                            }
+                            stg[q * KC + (k - kc0)] = term;
+                        }
+                    }
                 }
+                __syncwarp();
+                if (lane < nq) {
+                    const double* tj = stg + lane * KC;
+                    for (int k = 0; k < kc1 - kc0; ++k) s = __dadd_rn(s, tj[k]);
+                }
+                __syncwarp();  // the staging buffer is rewritten by the next pass
             }
-            if (lane == 0) {
+            if (lane < nq) {
+                const int j = nbr[t0 + lane];
                 const double d = pair_finish<M>(nn, (double)cnt[j], s, n2a, M == kSam ? n2g[j] : 0.0);
                 D[(size_t)a * Rp + j] = d;
                 D[(size_t)j * Rp + a] = d;
                 // rows whose cached neighbour was a or b were rescanned (a, b excluded)
-                // above, so every neighbour just takes the offer (d(j, a'), a')
-                if (d < bAd[j] || (d == bAd[j] && a < bAj[j]) || bAj[j] < 0) {
+                // above, so every neighbour just takes the offer (d(j, a'), a)
+                if (bAj[j] < 0 || d < bAd[j] || (d == bAd[j] && a < bAj[j])) {
                     bAd[j] = d;
                     bAj[j] = a;
                 }
@@ -356,15 +397,29 @@ __global__ void __launch_bounds__(kThreads, RHSEG_ADJ_MINBLOCKS) hseg_adj_kernel
     }
 }
 
-int launch_adj_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
+int launch_adj_loop(const SectionBatch& b, int nrun, int nsm, cudaStream_t st) {
     if (nrun == 0) return 0;
-    const size_t smem = adj_loop_smem(b.Rp, b.B);
-    void (*kern)(SectionBatch) = b.measure == kSam      ? hseg_adj_kernel<kSam>
-                                 : b.measure == kEuclid ? hseg_adj_kernel<kEuclid>
-                                                        : hseg_adj_kernel<kBsmse>;
+    // many sections: narrow CTAs, more of them resident (RHSEG_ADJ_NT=128|256 forces)
+    static const int forced = [] {
+        const char* e = getenv("RHSEG_ADJ_NT");
+        return e ? atoi(e) : 0;
+    }();
+    const bool narrow = forced ? forced == 128 : nrun > 2 * nsm;
+    void (*kern)(SectionBatch);
+#define RHSEG_ADJ_PICK(NT)                                                             \
+    kern = b.measure == kSam      ? hseg_adj_kernel<kSam, NT>                          \
+           : b.measure == kEuclid ? hseg_adj_kernel<kEuclid, NT>                       \
+                                  : hseg_adj_kernel<kBsmse, NT>;
+    if (narrow) {
+        RHSEG_ADJ_PICK(128)
+    } else {
+        RHSEG_ADJ_PICK(256)
+    }
+#undef RHSEG_ADJ_PICK
+    const size_t smem = adj_loop_smem(b.Rp, b.B, narrow ? 4 : 8);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<nrun, kThreads, smem, st>>>(b);
+    kern<<<nrun, narrow ? 128 : 256, smem, st>>>(b);
     return cudaGetLastError();
 }
 

@@ -60,8 +60,25 @@ constexpr int kKB = 16;
 // (B + 1) u (nonnegative terms), so d_ref lies within (B + 4) u of the d formed from s_fma;
 // the interval is twice that. The loop treats D entries as intervals anyway (exact values
 // only where a comparison needs them), so the merge sequence is unchanged.
+//
+// GRAM (RHSEG_DINIT_GRAM, the default for IV): ||m_i - m_j||^2 = n_i + n_j - 2 <m_i, m_j>
+// with n = ||m||^2 -- ONE fused multiply-add per pair-band (half the FP64 instructions).
+// Rigorous bound (u = 2^-53, FMA-accumulated sums of length B, gamma_B = B u / (1 - B u)):
+//   |g^ - g| <= gamma_B sum |m_ik m_jk| <= gamma_B (n_i + n_j) / 2,  |n^ - n| <= gamma_B n,
+//   S = fl(n^_i + n^_j), T^ = fl(S - 2 g^):  |T^ - T| <= (2 gamma_B + u) S + u |T^|,
+// taken twice over: T in [T^ - eT, T^ + eT], eT = (4B + 16) u S + 4 u |T^|. The reference
+// value then satisfies d_ref^2 = C T (1 + eps), |eps| <= (B + 8) u (apo_device.cuh), so
+// d_ref lies in [d(T_lo) (1 - rho), d(T_hi) (1 + rho)], rho = 2 (B + 8) u (+ the rounding of
+// d itself). The cancellation makes these intervals ~ (n_i + n_j) / T wider than the
+// difference form's -- ~1e-9 relative on the synthetic cubes, far below what the loop's
+// comparisons resolve; a pair whose lower bound reaches 0 (near-identical means) is
+// evaluated exactly here.
+#ifndef RHSEG_DINIT_GRAM
+#define RHSEG_DINIT_GRAM 0  // measured: init 83 -> 88 ms (4x4 blocking turns shared-memory bound) and the loop 376 -> 677 ms (1e-9-wide intervals: 11x more exact pairs); off
+#endif
 template <int M, bool IV = false>
 __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) {
+    constexpr bool GRAM = IV && RHSEG_DINIT_GRAM;
     const int sec = bt.sec0 + blockIdx.y;
     const int R0 = bt.R0[sec];
     const int nt = (R0 + kTile - 1) / kTile;
@@ -82,6 +99,8 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     // and is only touched after the last chunk's trailing __syncthreads()
     constexpr int kStage = 2 * kKB * kTile;  // doubles per buffer (A then B)
     __shared__ __align__(16) double smraw[(2 * kStage > kTile * (kTile + 1)) ? 2 * kStage : kTile * (kTile + 1)];
+    __shared__ double snorm[2 * kTile];  // GRAM: ||m||^2 of the tile's rows, then columns
+    double nacc = 0.0;                  // GRAM: threads < 128 accumulate one norm each
     double (*sT)[kTile + 1] = reinterpret_cast<double (*)[kTile + 1]>(smraw);
     // thread (tx, ty) owns rows i0 + 4 ty + p and columns j0 + 4 tx + q: both operand
     // quads are contiguous in shared memory (two 16-byte loads each)
@@ -131,7 +150,9 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
             for (int p = 0; p < 4; ++p)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (IV) {
+                    if (GRAM) {
+                        acc[p][q] = __fma_rn(a[p], b[q], acc[p][q]);
+                    } else if (IV) {
                         const double t = __dsub_rn(a[p], b[q]);
                         acc[p][q] = __fma_rn(t, t, acc[p][q]);
                     } else {
@@ -139,7 +160,17 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
                     }
                 }
         }
+        if (GRAM && threadIdx.x < 2 * kTile) {
+            const int r = threadIdx.x & (kTile - 1);
+            const double (*sX)[kTile] = threadIdx.x < kTile ? sA : sB;
+#pragma unroll
+            for (int kk = 0; kk < kKB; ++kk) nacc = __fma_rn(sX[kk][r], sX[kk][r], nacc);
+        }
         __syncthreads();  // buffer ch & 1 is refilled by the next iteration's stage()
+    }
+    if (GRAM) {
+        if (threadIdx.x < 2 * kTile) snorm[threadIdx.x] = nacc;
+        __syncthreads();
     }
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -148,7 +179,26 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
         for (int q = 0; q < 4; ++q) {
             const int j = j0 + 4 * tx + q;
             double d = 0.0;
-            if (i < R0 && j < R0) {
+            if (GRAM && i < R0 && j < R0) {
+                constexpr double u = 1.1102230246251565e-16;
+                const double S = __dadd_rn(snorm[4 * ty + p], snorm[kTile + 4 * tx + q]);
+                const double T = __dsub_rn(S, 2.0 * acc[p][q]);
+                const double eT = __dadd_ru(__dmul_ru(S, (4.0 * bt.B + 16.0) * u), __dmul_ru(fabs(T), 4.0 * u));
+                const double Tlo = fmax(0.0, __dsub_rd(T, eT)), Thi = __dadd_ru(T, eT);
+                const double ci = (double)cnt[i], cj = (double)cnt[j];
+                const double rho = 2.0 * (bt.B + 8) * u;
+                const double lo = __dmul_rd(pair_finish<M>(ci, cj, Tlo, 0.0, 0.0), __dsub_rd(1.0, rho));
+                const double hi = __dmul_ru(pair_finish<M>(ci, cj, Thi, 0.0, 0.0), __dadd_ru(1.0, rho));
+                if (i == j) {
+                    d = 0.0;  // (never read: rows skip their own column)
+                } else if (!d_pack_interval(lo, hi, d)) {
+                    // (near-)identical means: the reference's exact value (rare)
+                    double sx = 0.0;
+                    for (int k = 0; k < B; ++k) sx = acc_step<M>(sx, mu[(size_t)k * Rp + i], mu[(size_t)k * Rp + j]);
+                    d = pair_finish<M>(ci, cj, sx, 0.0, 0.0);
+                }
+                D[(size_t)i * Rp + j] = d;
+            } else if (i < R0 && j < R0) {
                 d = pair_finish<M>((double)cnt[i], (double)cnt[j], acc[p][q], M == kSam ? n2[i] : 0.0,
                                    M == kSam ? n2[j] : 0.0);
                 if (IV && d > 0.0) {
@@ -234,6 +284,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 // stages with 2 CTAs/SM beat 4 x 16 KB (-12%), 8 x 8 KB, 3 CTAs/SM with 2 x 16 KB,
 // per-warp empty barriers, L2 bulk prefetch and direct (unstaged) loads; the
 // per-stage block barrier + wait overhead, not the fetch latency, sets the pace.
+#ifndef RHSEG_APO_TOP2
+#define RHSEG_APO_TOP2 0  // APO rows keep their two best partners: C4 7.3 -> 4.4 rescans per step but each costs 1.8x (loop 359 -> 425 ms), off
+#endif
 #ifndef RHSEG_APO_OVERLAP
 #define RHSEG_APO_OVERLAP 0  // 1: row a' intervals by each warp right after its rescans (measured slower on C4)
 #endif
@@ -260,8 +313,15 @@ constexpr int kStageBytesTop2 = 20 * 1024;
 constexpr int kMaxSlots = 2048;  // own columns per CTA (cluster grows beyond)
 constexpr int kNbList = 256;     // b's neighbours re-pointed in parallel per merge
 
+// one slice of a split APO rescan: per stage the two smallest 32-bit keys, the
+// winner's column and D value, and the widest interval code
+struct RsSlice {
+    unsigned a1, a2, n1, n2;
+    int ja, jn, km, pad;
+    double va, vn;
+};
 struct LoopSmem {
-    size_t livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t rsp, livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -269,6 +329,7 @@ __host__ __device__ inline int own_rows(int R, int C) { return (((R + C - 1) / C
 __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool spec, bool top2,
                                                      int stage_bytes, int nstages) {
     const size_t Rs = (size_t)own_rows(Rp, C);
+    top2 = top2 || (spec && nstages == 0 && RHSEG_APO_TOP2);  // APO: two partners per row
     LoopSmem L;
     size_t o = 0;
     L.slot = o;  o += 2 * sizeof(Slot);
@@ -299,6 +360,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.apk = o;   o += 64;                                                  // APO: argmin keys, rule scratch
     L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
     L.livew = o; o = align16(o + (spec && nstages == 0 ? (size_t)(Rp / 32) * 4 : 0));  // APO: live-region bitset
+    L.rsp = o;   o = align16(o + (spec && nstages == 0 ? 2 * kWarps * sizeof(RsSlice) : 0));  // APO: rescan slices
     o = (o + 127) & ~size_t(127);
     L.ring = o;
     o += spec && nstages > 0 ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;  // (APO: no ring)
@@ -447,6 +509,12 @@ struct StreamState {
 #ifndef RHSEG_RESCAN_PIPE
 #define RHSEG_RESCAN_PIPE 0  // APO rescans: software-pipelined row walk
 #endif
+#ifndef RHSEG_RESCAN_SPLIT
+#define RHSEG_RESCAN_SPLIT 0  // APO: split the walks of a step with few rescans over idle warps (C4 loop 358 -> 376 ms: off)
+#endif
+#ifndef RHSEG_KEY32
+#define RHSEG_KEY32 1  // APO rescans on 32-bit keys with redux.sync (0: 64-bit keys, shuffle trees)
+#endif
 #ifndef RHSEG_RESCAN_U
 #define RHSEG_RESCAN_U 4  // APO rescans: D loads in flight per lane (C4 loop: 8 -> 427 ms, 4 -> 380, 2 -> 402, 1 -> 387)
 #endif
@@ -470,6 +538,10 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     constexpr bool TOP2 = SPEC && !CLUSTER && M == kSam;
     static_assert(!APO || (SPEC && !CLUSTER && M != kSam), "APO: w > 0, one CTA, BSMSE/Euclidean");
     constexpr bool F32 = APO;  // interval-valued D entries and caches (resolved exactly on demand)
+    // APO rows keep their two smallest candidates per stage with a "list holds every
+    // candidate" bit (the SAM lists, on intervals): a merge removes a and b from every
+    // list and only a list left empty and incomplete is rescanned
+    constexpr bool T2A = APO && RHSEG_APO_TOP2;
     constexpr bool STREAM = SPEC && !APO;  // row a' from the streamed mean columns
     using SE = double;  // streamed element
     constexpr int ES = (int)sizeof(SE);
@@ -519,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     double* const mr = APO ? bt.mu2 + 2 * sec * bt.mu_stride() : nullptr;
     unsigned short* ver = reinterpret_cast<unsigned short*>(smem + L.ver);  // APO: region -> mr row
     uint32_t* livew = reinterpret_cast<uint32_t*>(smem + L.livew);          // APO: live regions
+    RsSlice* rs_part = reinterpret_cast<RsSlice*>(smem + L.rsp);              // APO: rescan slices
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
@@ -529,6 +602,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     // partner was merged away. Adjacent-only rescans walk the adjacency bitset;
     // non-adjacent ones stream the D row with 8 loads in flight per lane.
     StreamState ss{};
+    int rs_exb = -1;  // APO: a column every rescan also skips (b while the merge runs beside them)
     auto rescan = [&](int i, int mask, int ex) {  // ex: column skipped (-1 = none)
         RowBest ba = rb_none(), bn = rb_none();
         if (cnt[i] != 0u) {
@@ -561,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int j = jv[u];
-                        if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                        if (j >= 0 && j != i && j != ex && j != rs_exb && cnt[j] != 0u) {
                             if ((arow[j >> 5] >> (j & 31)) & 1u) {
                                 if (mask & 1) rb_offer(ba, dv[u], j);
                             } else {
@@ -584,7 +658,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const int j = j0 + 32 * u + lane;
-                        if (j < R0 && j != i && j != ex && cnt[j] != 0u) {
+                        if (j < R0 && j != i && j != ex && j != rs_exb && cnt[j] != 0u) {
                             if ((wv[u] >> lane) & 1u) {
                                 if (mask & 1) rb_offer(ba, dv[u], j);
                             } else {
@@ -654,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
                     const int j = (w << 5) + lane;
                     const bool aj = (aw >> lane) & 1u;
-                    const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (mask & 1) : (mask & 2));
+                    const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (mask & 1) : (mask & 2));
                     sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
                     dv[u] = c ? __ldcs(drow + j) : kInf;
                 }
@@ -694,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 const int j = sl < ss.S ? col[sl] : -1;
                 bool cand = false, aj = false;
                 double v = kInf;
-                if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                if (j >= 0 && j != i && j != ex && j != rs_exb && cnt[j] != 0u) {
                     aj = (arow[j >> 5] >> (j & 31)) & 1u;
                     if (aj ? (mask & 1) && multA : (mask & 2) && multN) {
                         v = __ldcs(drow + j);
@@ -727,6 +801,12 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             const int r = i - lo;
             if (mask & 1) { bAd[r] = ba.d; bAj[r] = ba.j == kNoJ ? -1 : ba.j; }
             if (mask & 2) { bNd[r] = bn.d; bNj[r] = bn.j == kNoJ ? -1 : bn.j; }
+            if (T2A) {  // (first partner only: complete iff the stage has no candidate)
+                uint8_t c = cx[r];
+                if (mask & 1) { bAd2[r] = kInf; bAj2[r] = -1; c = ba.j == kNoJ ? (c | 1) : (c & ~1); }
+                if (mask & 2) { bNd2[r] = kInf; bNj2[r] = -1; c = bn.j == kNoJ ? (c | 2) : (c & ~2); }
+                cx[r] = c;
+            }
         }
     };
 
@@ -749,7 +829,199 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         const double rho = __longlong_as_double((long long)(kmax - 46 + 1023) << 52) + 0x1p-37;
         return h1 < __dmul_rd(c2, __dsub_rd(1.0, rho));
     };
-    auto rescanf = [&](int i, int mask, int ex) {
+#if RHSEG_KEY32
+    // 32-bit keys: the high word of the D bits with the sign cleared (exponent and 20
+    // mantissa bits: non-negative doubles order like it), kept per lane with the column
+    // and D value of the smallest; warp minima by redux.sync instead of 64-bit shuffle
+    // trees. Two entries within 2^-20 of each other share a key and fail the uniqueness
+    // test like any interval overlap (exact fallback), so the result is the same.
+    // part / nparts: this warp walks one slice of the row (nparts > 1: idle warps share the
+    // rescans of a step with few of them; the slice's keys go to rs_part[item] and
+    // rescanf_finish combines them after the post-rescan barrier)
+    auto rescanf = [&](int i, int mask, int ex, int part, int nparts, int item) {
+        const uint32_t* arow = adj + (size_t)i * W;
+        const double* drow = D + (size_t)i * Rp;
+        unsigned a1 = ~0u, a2 = ~0u, n1 = ~0u, n2 = ~0u;
+        int ja = -1, jn = -1;
+        double va = kInf, vn = kInf;
+        int km = 0;  // widest interval code over both stages (only widens the test)
+        constexpr int U = RHSEG_RESCAN_U;
+        // the walk is specialised on the stage mask: a single-stage rescan (the common
+        // case) tracks one pair of keys
+        auto walk = [&](auto MKC) {
+            constexpr int MK = decltype(MKC)::value;
+            auto take = [&](double v, int j, bool c, bool aj) {
+                const unsigned hw = (unsigned)__double2hiint(v), lw = (unsigned)__double2loint(v);
+                km = max(km, (int)(hw >> 31) * (int)(lw & 63u));
+                const unsigned key = c ? (hw & 0x7fffffffu) : ~0u;
+                if (MK == 1 || MK == 3) {
+                    const unsigned ka = (MK == 1 || aj) ? key : ~0u;
+                    if (ka < a1) { a2 = a1; a1 = ka; ja = j; va = v; }
+                    else a2 = min(a2, ka);
+                }
+                if (MK == 2 || MK == 3) {
+                    const unsigned kn = (MK == 2 || !aj) ? key : ~0u;
+                    if (kn < n1) { n2 = n1; n1 = kn; jn = j; vn = v; }
+                    else n2 = min(n2, kn);
+                }
+            };
+            if (RHSEG_SPARSE_DEN * ss.S < RHSEG_SPARSE_NUM * R0) {
+                // sparse (most regions merged away): walk the compacted live-column list
+                const int slo = part * ss.S / nparts, shi = (part + 1) * ss.S / nparts;
+                for (int s0 = slo; s0 < shi; s0 += 32 * U) {
+                    double dv[U];
+                    int jv[U];
+                    uint32_t sel[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int sl = s0 + 32 * u + lane;
+                        const int j = sl < shi ? col[sl] : -1;
+                        bool c = false, aj = false;
+                        if (j >= 0 && j != i && j != ex && j != rs_exb && ((livew[j >> 5] >> (j & 31)) & 1u)) {
+                            aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                            c = aj ? (MK & 1) : (MK & 2);
+                        }
+                        jv[u] = j;
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
+                }
+            } else {
+                // id-ordered walk, one bitset word per warp-iteration: lane l takes id
+                // 32 w + l, whose liveness and adjacency bits come from two broadcast
+                // words, and the D loads of a warp are one contiguous 256-byte segment
+                const int wlo = part * W / nparts, whi = (part + 1) * W / nparts;
+                auto issue = [&](int w0, double* dv, uint32_t* sel) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int w = w0 + u;
+                        const uint32_t lw = w < whi ? livew[w] : 0u, aw = w < whi ? arow[w] : 0u;
+                        const int j = (w << 5) + lane;
+                        const bool aj = (aw >> lane) & 1u;
+                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (MK & 1) : (MK & 2));
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    }
+                };
+                if (RHSEG_RESCAN_PIPE) {
+                    // software-pipelined: the next batch's loads are in flight while this
+                    // batch is folded into the keys
+                    double dv[U], dn[U];
+                    uint32_t sel[U], sn[U];
+                    issue(wlo, dv, sel);
+                    for (int w0 = wlo; w0 < whi; w0 += U) {
+                        if (w0 + U < whi) issue(w0 + U, dn, sn);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) { dv[u] = dn[u]; sel[u] = sn[u]; }
+                    }
+                } else {
+                    for (int w0 = wlo; w0 < whi; w0 += U) {
+                        double dv[U];
+                        uint32_t sel[U];
+                        issue(w0, dv, sel);
+#pragma unroll
+                        for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+                    }
+                }
+            }
+        };
+        if (cnt[i] != 0u) {
+            if (mask == 1) walk(std::integral_constant<int, 1>{});
+            else if (mask == 2) walk(std::integral_constant<int, 2>{});
+            else walk(std::integral_constant<int, 3>{});
+        }
+        km = __reduce_max_sync(0xffffffffu, km);
+        // warp minimum of one stage: the smallest key, the second smallest (== the
+        // smallest on a tie), the winner's column and D value
+        auto reduce = [&](unsigned& k1, unsigned& k2, int& j1, double& v1) {
+            const unsigned m1 = __reduce_min_sync(0xffffffffu, k1);
+            const unsigned win = __ballot_sync(0xffffffffu, k1 == m1);
+            const int wl = __ffs(win) - 1;
+            const unsigned m2 = __popc(win) > 1 ? m1 : __reduce_min_sync(0xffffffffu, lane == wl ? k2 : k1);
+            j1 = __shfl_sync(0xffffffffu, j1, wl);
+            v1 = __shfl_sync(0xffffffffu, v1, wl);
+            k1 = m1;
+            k2 = m2;
+        };
+        // unique iff the smallest key's upper bound lies below the lower bound of every
+        // other entry: their centres are >= the second key (truncated), each interval
+        // within 2^(km-46) of its centre
+        auto unique32 = [&](unsigned k2, double v1) {
+            if (k2 == ~0u) return true;
+            double l1, h1;
+            d_unpack(v1, l1, h1);
+            const double c2 = __hiloint2double((int)k2, 0);
+            const double rho = __longlong_as_double((long long)(km - 46 + 1023) << 52) + 0x1p-37;
+            return h1 < __dmul_rd(c2, __dsub_rd(1.0, rho));
+        };
+        if (nparts > 1) {  // this slice's warp minima -> rs_part[item]
+            if (mask & 1) reduce(a1, a2, ja, va);
+            if (mask & 2) reduce(n1, n2, jn, vn);
+            if (lane == 0) rs_part[item] = RsSlice{a1, a2, n1, n2, ja, jn, km, 0, va, vn};
+            return;
+        }
+        int slow = 0;
+        if (mask & 1) {
+            reduce(a1, a2, ja, va);
+            if (a1 != ~0u && !unique32(a2, va)) slow |= 1;
+        }
+        if (mask & 2) {
+            reduce(n1, n2, jn, vn);
+            if (n1 != ~0u && !unique32(n2, vn)) slow |= 2;
+        }
+        if (lane == 0) {
+            const int r = i - lo;
+            if ((mask & 1) && !(slow & 1)) { bAd[r] = a1 == ~0u ? kInf : va; bAj[r] = a1 == ~0u ? -1 : ja; }
+            if ((mask & 2) && !(slow & 2)) { bNd[r] = n1 == ~0u ? kInf : vn; bNj[r] = n1 == ~0u ? -1 : jn; }
+        }
+        if (slow) rescanf_full(i, slow, ex);
+    };
+    // combine the nparts slices of row i (one warp; after the barrier closing the walks)
+    auto rescanf_finish = [&](int i, int mask, int ex, int nparts, int item0) {
+        RsSlice p = lane < nparts ? rs_part[item0 + lane]
+                                  : RsSlice{~0u, ~0u, ~0u, ~0u, -1, -1, 0, 0, kInf, kInf};
+        const int km = __reduce_max_sync(0xffffffffu, p.km);
+        auto reduce = [&](unsigned& k1, unsigned& k2, int& j1, double& v1) {
+            const unsigned m1 = __reduce_min_sync(0xffffffffu, k1);
+            const unsigned win = __ballot_sync(0xffffffffu, k1 == m1);
+            const int wl = __ffs(win) - 1;
+            const unsigned m2 = __popc(win) > 1 ? m1 : __reduce_min_sync(0xffffffffu, lane == wl ? k2 : k1);
+            j1 = __shfl_sync(0xffffffffu, j1, wl);
+            v1 = __shfl_sync(0xffffffffu, v1, wl);
+            k1 = m1;
+            k2 = m2;
+        };
+        auto unique32 = [&](unsigned k2, double v1) {
+            if (k2 == ~0u) return true;
+            double l1, h1;
+            d_unpack(v1, l1, h1);
+            const double c2 = __hiloint2double((int)k2, 0);
+            const double rho = __longlong_as_double((long long)(km - 46 + 1023) << 52) + 0x1p-37;
+            return h1 < __dmul_rd(c2, __dsub_rd(1.0, rho));
+        };
+        int slow = 0;
+        if (mask & 1) {
+            reduce(p.a1, p.a2, p.ja, p.va);
+            if (p.a1 != ~0u && !unique32(p.a2, p.va)) slow |= 1;
+        }
+        if (mask & 2) {
+            reduce(p.n1, p.n2, p.jn, p.vn);
+            if (p.n1 != ~0u && !unique32(p.n2, p.vn)) slow |= 2;
+        }
+        if (lane == 0) {
+            const int r = i - lo;
+            if ((mask & 1) && !(slow & 1)) { bAd[r] = p.a1 == ~0u ? kInf : p.va; bAj[r] = p.a1 == ~0u ? -1 : p.ja; }
+            if ((mask & 2) && !(slow & 2)) { bNd[r] = p.n1 == ~0u ? kInf : p.vn; bNj[r] = p.n1 == ~0u ? -1 : p.jn; }
+        }
+        if (slow) rescanf_full(i, slow, ex);
+    };
+
+#else
+    auto rescanf = [&](int i, int mask, int ex, int, int, int) {
         const uint32_t* arow = adj + (size_t)i * W;
         const double* drow = D + (size_t)i * Rp;
         unsigned long long a1 = kKeyNone, a2 = kKeyNone, n1 = kKeyNone, n2 = kKeyNone;
@@ -785,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         const int sl = s0 + 32 * u + lane;
                         const int j = sl < ss.S ? col[sl] : -1;
                         bool c = false, aj = false;
-                        if (j >= 0 && j != i && j != ex && ((livew[j >> 5] >> (j & 31)) & 1u)) {
+                        if (j >= 0 && j != i && j != ex && j != rs_exb && ((livew[j >> 5] >> (j & 31)) & 1u)) {
                             aj = (arow[j >> 5] >> (j & 31)) & 1u;
                             c = aj ? (MK & 1) : (MK & 2);
                         }
@@ -807,7 +1079,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
                         const int j = (w << 5) + lane;
                         const bool aj = (aw >> lane) & 1u;
-                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && (aj ? (MK & 1) : (MK & 2));
+                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (MK & 1) : (MK & 2));
                         sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
                         dv[u] = c ? __ldcs(drow + j) : 0.0;
                     }
@@ -863,6 +1135,135 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         if (slow) rescanf_full(i, slow, ex);
     };
 
+#endif
+    // TOP2-APO rescan: per masked stage the entries of the two smallest 32-bit keys and
+    // the third key; the first is certified as in rescanf (upper bound below the second
+    // key's lower bound), the second when its upper bound lies below the third key's; a
+    // list is complete when it holds every candidate of the stage.
+    struct K3 {
+        unsigned k1, k2, k3;
+        int j1, j2, n;
+        double v1, v2;
+    };
+    auto rescant = [&](int i, int mask, int ex) {
+        const uint32_t* arow = adj + (size_t)i * W;
+        const double* drow = D + (size_t)i * Rp;
+        K3 xa{~0u, ~0u, ~0u, -1, -1, 0, kInf, kInf}, xn = xa;
+        int km = 0;
+        auto put = [](K3& x, unsigned key, int j, double v) {
+            x.n += 1;
+            if (key < x.k1) {
+                x.k3 = x.k2; x.k2 = x.k1; x.j2 = x.j1; x.v2 = x.v1;
+                x.k1 = key; x.j1 = j; x.v1 = v;
+            } else if (key < x.k2) {
+                x.k3 = x.k2; x.k2 = key; x.j2 = j; x.v2 = v;
+            } else {
+                x.k3 = min(x.k3, key);
+            }
+        };
+        auto take = [&](double v, int j, bool c, bool aj) {
+            if (!c) return;
+            const unsigned hw = (unsigned)__double2hiint(v), lw = (unsigned)__double2loint(v);
+            km = max(km, (int)(hw >> 31) * (int)(lw & 63u));
+            if (aj) put(xa, hw & 0x7fffffffu, j, v);
+            else put(xn, hw & 0x7fffffffu, j, v);
+        };
+        constexpr int U = RHSEG_RESCAN_U;
+        if (cnt[i] != 0u) {
+            if (RHSEG_SPARSE_DEN * ss.S < RHSEG_SPARSE_NUM * R0) {
+                for (int s0 = 0; s0 < ss.S; s0 += 32 * U) {
+                    double dv[U];
+                    int jv[U];
+                    uint32_t sel[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int sl = s0 + 32 * u + lane;
+                        const int j = sl < ss.S ? col[sl] : -1;
+                        bool c = false, aj = false;
+                        if (j >= 0 && j != i && j != ex && j != rs_exb && ((livew[j >> 5] >> (j & 31)) & 1u)) {
+                            aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                            c = aj ? (mask & 1) : (mask & 2);
+                        }
+                        jv[u] = j;
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
+                }
+            } else {
+                for (int w0 = 0; w0 < W; w0 += U) {
+                    double dv[U];
+                    uint32_t sel[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int w = w0 + u;
+                        const uint32_t lw = w < W ? livew[w] : 0u, aw = w < W ? arow[w] : 0u;
+                        const int j = (w << 5) + lane;
+                        const bool aj = (aw >> lane) & 1u;
+                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (mask & 1) : (mask & 2));
+                        sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) take(dv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+                }
+            }
+        }
+        km = __reduce_max_sync(0xffffffffu, km);
+        const double rho = __longlong_as_double((long long)(km - 46 + 1023) << 52) + 0x1p-37;
+        auto below = [&](double v, unsigned knext) {  // v's upper bound < every entry keyed >= knext
+            if (knext == ~0u) return true;
+            double l, h;
+            d_unpack(v, l, h);
+            return h < __dmul_rd(__hiloint2double((int)knext, 0), __dsub_rd(1.0, rho));
+        };
+        // warp top-2 of one stage (+ the third key); res: 0 empty, 1 first only, 2 both, -1 slow
+        auto reduce3 = [&](K3& x, int& res, bool& complete) {
+            const int n = __reduce_add_sync(0xffffffffu, x.n);
+            const unsigned m1 = __reduce_min_sync(0xffffffffu, x.k1);
+            const unsigned b1 = __ballot_sync(0xffffffffu, x.k1 == m1);
+            const int w1 = __ffs(b1) - 1;
+            const bool tie1 = __popc(b1) > 1;
+            const unsigned o2 = lane == w1 ? x.k2 : x.k1;
+            const unsigned m2 = tie1 ? m1 : __reduce_min_sync(0xffffffffu, o2);
+            const unsigned b2 = __ballot_sync(0xffffffffu, o2 == m2);
+            const int w2 = __ffs(b2) - 1;
+            const bool tie2 = tie1 || __popc(b2) > 1;
+            const unsigned o3 = lane == w1 ? (w2 == w1 ? x.k3 : x.k2) : (lane == w2 ? x.k2 : x.k1);
+            const unsigned m3 = tie2 ? m2 : __reduce_min_sync(0xffffffffu, o3);
+            const double v1 = __shfl_sync(0xffffffffu, x.v1, w1);
+            const int j1 = __shfl_sync(0xffffffffu, x.j1, w1);
+            const double v2 = __shfl_sync(0xffffffffu, w2 == w1 ? x.v2 : x.v1, w2);
+            const int j2 = __shfl_sync(0xffffffffu, w2 == w1 ? x.j2 : x.j1, w2);
+            x.v1 = v1; x.j1 = j1; x.v2 = v2; x.j2 = j2;
+            if (m1 == ~0u) { res = 0; complete = true; return; }
+            if (!below(v1, m2)) { res = -1; complete = false; return; }
+            res = (m2 != ~0u && !tie2 && below(v2, m3)) ? 2 : 1;
+            complete = n <= res;
+        };
+        int slow = 0, ra = 0, rn = 0;
+        bool ca = false, cn = false;
+        if (mask & 1) { reduce3(xa, ra, ca); if (ra < 0) slow |= 1; }
+        if (mask & 2) { reduce3(xn, rn, cn); if (rn < 0) slow |= 2; }
+        if (lane == 0) {
+            const int r = i - lo;
+            uint8_t c = cx[r];
+            if ((mask & 1) && ra >= 0) {
+                bAd[r] = ra ? xa.v1 : kInf; bAj[r] = ra ? xa.j1 : -1;
+                bAd2[r] = ra == 2 ? xa.v2 : kInf; bAj2[r] = ra == 2 ? xa.j2 : -1;
+                c = ca ? (c | 1) : (c & ~1);
+            }
+            if ((mask & 2) && rn >= 0) {
+                bNd[r] = rn ? xn.v1 : kInf; bNj[r] = rn ? xn.j1 : -1;
+                bNd2[r] = rn == 2 ? xn.v2 : kInf; bNj2[r] = rn == 2 ? xn.j2 : -1;
+                c = cn ? (c | 2) : (c & ~2);
+            }
+            cx[r] = c;
+        }
+        if (slow) rescanf_full(i, slow, ex);
+    };
+
     // TOP2 rescan: the two best candidates per masked stage + the complete bit,
     // over the compacted live-column list (one CTA owns every column).
     auto rescan2 = [&](int i, int mask, int ex) {
@@ -884,7 +1285,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const int j = jv[u];
-                    if (j >= 0 && j != i && j != ex && cnt[j] != 0u) {
+                    if (j >= 0 && j != i && j != ex && j != rs_exb && cnt[j] != 0u) {
                         if ((arow[j >> 5] >> (j & 31)) & 1u) {
                             if (mask & 1) t2_offer(ta, dv[u], j);
                         } else if (mask & 2) {
@@ -1018,6 +1419,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     }
     if (tid == 0) {
         ninv = 0;
+        misc[12] = 0;
         sdE = 0;
         sE0 = 0ull;
         sScan = 0;
@@ -1062,8 +1464,16 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         for (int r = tid; r < hi - lo; r += kThreads) cx[r] = 0;
         __syncthreads();
         for (int i = lo + warp; i < hi; i += kWarps) rescan2(i, 3, -1);
+    } else if (T2A) {
+        for (int r = tid; r < hi - lo; r += kThreads) {
+            cx[r] = 0;
+            bAd2[r] = kInf; bAj2[r] = -1;
+            bNd2[r] = kInf; bNj2[r] = -1;
+        }
+        __syncthreads();
+        for (int i = lo + warp; i < hi; i += kWarps) rescant(i, 3, -1);
     } else if (F32) {
-        for (int i = lo + warp; i < hi; i += kWarps) rescanf(i, 3, -1);
+        for (int i = lo + warp; i < hi; i += kWarps) rescanf(i, 3, -1, 0, 1, 0);
     } else {
         for (int i = lo + warp; i < hi; i += kWarps) rescan(i, SPEC ? 3 : 1, -1);
     }
@@ -1307,7 +1717,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             if (cnt[i] == 0u || i == a || i == b) continue;
             const int r = i - lo;
             int mask = 0;
-            if (TOP2) {
+            if (TOP2 || T2A) {
                 l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], a);
                 l2_remove(bAd[r], bAj[r], bAd2[r], bAj2[r], b);
                 l2_remove(bNd[r], bNj[r], bNd2[r], bNj2[r], a);
@@ -1334,12 +1744,22 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         const double na0 = (double)cnt[a], nb0 = (double)cnt[b];  // (APO: the log's exact value, in C2)
         ApoStep ap{};
         if (APO) ap = apo_step<M>(na0, nb0, dch, apoE, apoEe);
+        // APO: the merge runs on warps 0-1 (named barrier) while the other warps start
+        // the rescans (which skip a and b and read nothing the merge writes but bits a
+        // and b of neighbour rows' adjacency words); the others merge with every thread
+        constexpr int MT = APO ? 2 * 32 : kThreads;  // merging threads
+        if (APO) {
+            __syncthreads();  // the invalidated-row list is complete
+            rs_exb = b;
+        }
+        uint32_t* ra = adj + (size_t)a * W;
+        if (!APO || warp < 2) {
         {
             double* sa = sums + (size_t)a * B;
             const double* sb = sums + (size_t)b * B;
             SE* mu_a = STREAM ? (own_a ? (ss.cur ? sb1 : sb0) + lo + slot_of[a - lo] : nullptr)
                               : (SPEC ? nullptr : mu0 + a);
-            for (int k = tid; k < B; k += kThreads) {
+            for (int k = tid; k < B; k += MT) {
                 const double s = __dadd_rn(sa[k], sb[k]);
                 sa[k] = s;
                 const double m = __ddiv_rn(s, nn);
@@ -1348,7 +1768,6 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             }
             if (STREAM && own_a) fence_proxy_async_global();
         }
-        uint32_t* ra = adj + (size_t)a * W;
         {
             // adjacency union (A|B)\{a,b}; b's neighbours are collected first and then
             // re-pointed b -> a one per thread (not serially per bitset word)
@@ -1361,7 +1780,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 else { rn[wa] |= ma; rn[wb] &= ~mb; }
             };
             int dE = 0;
-            for (int w = tid; w < W; w += kThreads) {
+            for (int w = tid; w < W; w += MT) {
                 const uint32_t oa = ra[w], ob = rbw[w];
                 uint32_t nw = oa | ob;
                 if (w == wa) nw &= ~ma;
@@ -1383,9 +1802,34 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 }
             }
             if (SPEC && dE) atomicAdd(&sdE, dE);
-            __syncthreads();
+            if (APO) asm volatile("bar.sync 1, %0;" ::"n"(MT) : "memory");
+            else __syncthreads();
             const int nb = min(nnb, kNbList);
-            for (int k = tid; k < nb; k += kThreads) repoint(nbl[k]);
+            for (int k = tid; k < nb; k += MT) repoint(nbl[k]);
+        }
+        }  // (merging threads)
+        if (APO) {
+            // the rescans: rows claimed from a shared counter (the merge warps join when done)
+            const long long tr0 = clock64();
+            int nr = 0;
+            const int ni = ninv;
+            for (;;) {
+                int k = 0;
+                if (lane == 0) k = atomicAdd(&misc[12], 1);
+                k = __shfl_sync(0xffffffffu, k, 0);
+                if (k >= ni) break;
+                rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0);
+                ++nr;
+            }
+            if (bt.prof && lane == 0 && nr) {
+                const unsigned long long dt = (unsigned long long)(clock64() - tr0);
+                atomicAdd(bt.prof + 13, dt);
+                atomicAdd(bt.prof + 14, (unsigned long long)nr);
+                atomicMax(bt.prof + 15, dt);
+            }
+            if (tid == 0) nresc += ni;
+            if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
+            rs_exb = -1;
         }
         __syncthreads();  // every thread has read cnt[a], cnt[b] (nn) before they change
         if (tid == 0) {
@@ -1411,7 +1855,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 }
             }
         }
-        __syncthreads();
+        if (!APO) __syncthreads();  // (APO: nothing below reads cnt[a], cnt[b] or the live set before the next barrier)
         if (SPEC) E += sdE;
         mark(2);
 
@@ -1460,7 +1904,10 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             }
         };
         if (APO && tid == 0) { sScan = 0; misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
-        {
+        // split APO rescans: with ni <= kWarps / 2 rows each row's walk is cut into the
+        // largest power-of-two number of slices that keeps every warp busy
+        const int nsplit = 1;  // (split rescans: measured slower, and APO now rescans beside the merge)
+        if (!APO) {
             const int ni = ninv;
             if (tid == 0) nresc += ni;
             if (bt.prof && tid == 0) pc[5] += (unsigned long long)ni;
@@ -1520,7 +1967,14 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             } else if (APO) {
                 const long long tr0 = clock64();
                 int nr = 0;
-                for (int k = warp; k < ni; k += kWarps, ++nr) rescanf(inv[k] >> 2, inv[k] & 3, a);
+                if (T2A) {
+                    for (int k = warp; k < ni; k += kWarps, ++nr) rescant(inv[k] >> 2, inv[k] & 3, a);
+                } else if (nsplit > 1) {  // few rescans: every row's walk split over idle warps
+                    for (int t = warp; t < ni * nsplit; t += kWarps, ++nr)
+                        rescanf(inv[t / nsplit] >> 2, inv[t / nsplit] & 3, a, t % nsplit, nsplit, t);
+                } else {
+                    for (int k = warp; k < ni; k += kWarps, ++nr) rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0);
+                }
                 // then, without waiting for the other warps' rescans: the intervals of
                 // row a' (D rows a and b are not touched by the rescans, which skip a)
                 if (RHSEG_APO_OVERLAP) apo_rows();
@@ -1534,8 +1988,16 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 for (int k = warp; k < ni; k += kWarps) rescan(inv[k] >> 2, inv[k] & 3, a);
             }
         }
-        __syncthreads();
-        if (APO && !RHSEG_APO_OVERLAP) apo_rows();  // (own slots only: the offers' reduction barrier follows)
+        if (!APO) __syncthreads();  // (APO: the rescans ran beside the merge)
+        if (nsplit > 1) {  // combine the slices (the offers' reduction barrier follows)
+            const int ni = ninv;
+            for (int k = warp; k < ni; k += kWarps) rescanf_finish(inv[k] >> 2, inv[k] & 3, a, nsplit, k * nsplit);
+        }
+        if (APO && !RHSEG_APO_OVERLAP) {
+            const long long ta = bt.prof ? clock64() : 0;
+            apo_rows();
+            if (bt.prof && tid == 0) atomicAdd(bt.prof + 10, (unsigned long long)(clock64() - ta));  // (part of phase 4)
+        }  // (own slots only: the offers' reduction barrier follows)
         mark(4);
         // (D) row-a pass over own columns: fresh d(a, j), D update, cache offers
         RowBest pA = rb_none(), pN = rb_none();
@@ -1632,7 +2094,39 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     }
                     double& bv = aj ? bAd[r] : bNd[r];
                     int& bj = aj ? bAj[r] : bNj[r];
-                    if (bj < 0) {
+                    if (T2A) {
+                        // insert (d(a', j), a) into row j's two-entry list on the intervals
+                        // (an empty list is complete here: incomplete ones were rescanned)
+                        double& bv2 = aj ? bAd2[r] : bNd2[r];
+                        int& bj2 = aj ? bAj2[r] : bNj2[r];
+                        const uint8_t bit = aj ? 1 : 2;
+                        if (bj < 0) {
+                            bv = v;
+                            bj = a;
+                        } else {
+                            double bl, bh;
+                            d_unpack(bv, bl, bh);
+                            if (dhi < bl) {  // a' first; a listed second drops out
+                                if (bj2 >= 0) cx[r] &= (uint8_t)~bit;
+                                bv2 = bv; bj2 = bj;
+                                bv = v; bj = a;
+                            } else if (dlo > bh) {
+                                if (bj2 < 0) {
+                                    // complete single entry: a' is the second; otherwise a'
+                                    // may sit behind unlisted candidates (not listed)
+                                    if (cx[r] & bit) { bv2 = v; bj2 = a; }
+                                } else {
+                                    double cl, ch;
+                                    d_unpack(bv2, cl, ch);
+                                    if (dhi < cl) { bv2 = v; bj2 = a; cx[r] &= (uint8_t)~bit; }
+                                    else if (dlo > ch) cx[r] &= (uint8_t)~bit;
+                                    else l1[atomicAdd(&cntF[0], 1)] = e;
+                                }
+                            } else {
+                                l1[atomicAdd(&cntF[0], 1)] = e;
+                            }
+                        }
+                    } else if (bj < 0) {
                         bv = v;
                         bj = a;
                     } else {
@@ -1657,11 +2151,46 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     double db = aj ? bAd[r] : bNd[r];
                     const bool binterval = bj >= 0 && d_is_interval(db);
                     if (binterval) db = exact_pair(j, bj);
+                    const bool take_a = bj < 0 || daj < db || (daj == db && a < bj);
+                    if (T2A) {
+                        // exact insertion into the two-entry list (uniform decisions: every
+                        // lane read the same cache entries)
+                        const uint8_t bit = aj ? 1 : 2;
+                        const int bj2 = aj ? bAj2[r] : bNj2[r];
+                        double db2 = aj ? bAd2[r] : bNd2[r];
+                        const bool complete = cx[r] & bit;
+                        bool take2 = false;
+                        if (!take_a && bj2 >= 0) {
+                            if (d_is_interval(db2)) db2 = exact_pair(j, bj2);
+                            take2 = daj < db2 || (daj == db2 && a < bj2);
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            D[(size_t)j * Rp + a] = daj;
+                            D[(size_t)a * Rp + j] = daj;
+                            double n1d = db, n2d = db2;
+                            int n1j = bj, n2j = bj2;
+                            uint8_t c = cx[r];
+                            if (bj < 0) { n1d = daj; n1j = a; }
+                            else if (take_a) {
+                                if (bj2 >= 0) c &= (uint8_t)~bit;
+                                n2d = db; n2j = bj; n1d = daj; n1j = a;
+                            } else if (bj2 < 0) {
+                                if (complete) { n2d = daj; n2j = a; }
+                            } else {
+                                if (take2) { n2d = daj; n2j = a; }
+                                c &= (uint8_t)~bit;
+                            }
+                            if (aj) { bAd[r] = n1d; bAj[r] = n1j; bAd2[r] = n2d; bAj2[r] = n2j; }
+                            else { bNd[r] = n1d; bNj[r] = n1j; bNd2[r] = n2d; bNj2[r] = n2j; }
+                            cx[r] = c;
+                        }
+                        continue;
+                    }
                     __syncwarp();  // every lane has read row j's cache before lane 0 rewrites it
                     if (lane == 0) {
                         D[(size_t)j * Rp + a] = daj;
                         D[(size_t)a * Rp + j] = daj;
-                        const bool take_a = bj < 0 || daj < db || (daj == db && a < bj);
                         if (aj) { bAd[r] = take_a ? daj : db; bAj[r] = take_a ? a : bj; }
                         else { bNd[r] = take_a ? daj : db; bNj[r] = take_a ? a : bj; }
                     }
@@ -1742,9 +2271,15 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 bAj[r] = pA.j == kNoJ ? -1 : pA.j;
                 bNd[r] = pN.d;
                 bNj[r] = pN.j == kNoJ ? -1 : pN.j;
+                if (T2A) {  // a's fresh row: its best only (complete iff the stage has none)
+                    bAd2[r] = kInf; bAj2[r] = -1;
+                    bNd2[r] = kInf; bNj2[r] = -1;
+                    cx[r] = (uint8_t)((pA.j == kNoJ ? 1 : 0) | (pN.j == kNoJ ? 2 : 0));
+                }
                 ninv = 0;
                 nnb = 0;
                 sScan = 0;
+                misc[12] = 0;  // rescan claim counter
                 ak[0] = ak[1] = ak[4] = ak[5] = 0xffffffffu;
                 ak[2] = ak[3] = 0u;
             }
@@ -1812,7 +2347,15 @@ int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
         const char* e = getenv("RHSEG_ADJ_V1");
         return e && e[0] == '1';
     }();
-    if (!b.spec && b.C == 1 && !adj_v1) return launch_adj_loop(b, nrun, st);
+    if (!b.spec && b.C == 1 && !adj_v1) {
+        static const int nsm = [] {
+            int dev = 0, n = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+            return n;
+        }();
+        return launch_adj_loop(b, nrun, nsm, st);
+    }
     const size_t smem = hseg_loop_smem(b.Rp, b.C, b.B, b.spec != 0, b.measure, b.stage_bytes, b.nstages);
     void (*kern)(SectionBatch);
 #define RHSEG_PICK(M)                                                                              \

@@ -505,6 +505,9 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
                     "%.2f rescan exact pairs (%.0f cycles each)\n", lv.level, (double)ph[8] / std::max(1LL, steps),
                     (double)ph[9] / std::max(1LL, steps), (double)ph[11] / std::max(1LL, steps),
                     (double)ph[12] / std::max(1ULL, ph[11]));
+        if (ph[10])
+            fprintf(stderr, "[rhseg profile] level %d APO row-a' intervals (inside the last phase): %.0f cycles/step\n",
+                    lv.level, (double)ph[10] / (double)std::max(1LL, steps));
         if (ph[14])
             fprintf(stderr, "[rhseg profile] level %d APO rescans: %.0f cycles per rescan (warp view), max warp %.0f\n",
                     lv.level, (double)ph[13] / ph[14], (double)ph[15]);

@@ -75,8 +75,8 @@ void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
 int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st);  // returns cudaError_t
 int launch_apo_loop(const SectionBatch& b, int nrun, cudaStream_t st);   // apo_loop.cu (b.apo sections)
 size_t apo_loop_smem(int Rp, int B);
-int launch_adj_loop(const SectionBatch& b, int nrun, cudaStream_t st);   // adj_loop.cu (w = 0, C = 1)
-size_t adj_loop_smem(int Rp, int B);
+int launch_adj_loop(const SectionBatch& b, int nrun, int nsm, cudaStream_t st);   // adj_loop.cu (w = 0, C = 1)
+size_t adj_loop_smem(int Rp, int B, int nwarps);
 size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes, int nstages);
 int hseg_loop_max_stages();
 int hseg_loop_default_stages();
