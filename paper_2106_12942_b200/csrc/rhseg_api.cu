@@ -234,9 +234,12 @@ static void reset_ctx(rhseg_ctx* c, cudaStream_t st) {
     memset(&c->info, 0, sizeof(c->info));
 }
 
-static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced) {
+static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced, bool apo_ok) {
     if (forced > 0) return forced;
     if (R0max < 512) return 1;
+    // sections the one-CTA APO loop can hold run there even when few: C2's 16 leaves of
+    // 1296 regions, 46.5 ms on 4-CTA clusters (mean stream) -> 33.1 ms (profiles/r02_experiments)
+    if (apo_ok && R0max <= hseg_loop_max_rows()) return 1;
     int C = 1;
     while (C * 2 <= kMaxCluster && nsec * C * 2 <= c->nsm && R0max / (C * 2) >= 128) C *= 2;
     return C;
@@ -251,8 +254,12 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
                                            std::to_string(kMaxSectionRegions));
     lv.Rp = std::max(64, (lv.R0max + 63) / 64 * 64);
     lv.W = lv.Rp / 32;
-    lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C);
     const bool spec = weight > 0.0;
+    {
+        const char* apo_env = getenv("RHSEG_APO");
+        const bool apo_ok = hseg_apo_capable(spec, 1, lv.measure) && !(apo_env && apo_env[0] == '0');
+        lv.C = choose_cluster(c, lv.nsec, lv.R0max, forced_C, apo_ok);
+    }
     auto fits = [&](int C) {
         return hseg_loop_smem(lv.Rp, C, lv.B, spec, lv.measure, hseg_loop_stage_bytes(spec, C, lv.measure),
                               hseg_loop_default_stages()) <=

@@ -21,12 +21,13 @@ from bench import MEASURE_OF, WORKLOADS, _phase_ms_of, make_cube  # noqa: E402
 def main():
     args = sys.argv[1:]
     timing = "--time" in args
+    cluster = int(os.environ.get("RHSEG_CLUSTER", "0"))  # forced CTAs per section (0 = auto)
     names = [a for a in args if not a.startswith("--")]
     for name in names:
         spec, crop, levels, w, t, st = WORKLOADS[name]
         cube = torch.from_numpy(np.ascontiguousarray(make_cube(name))).cuda()
         bands, edge, _ = cube.shape
-        ex = rh.B200Executor(device=0)
+        ex = rh.B200Executor(device=0, cluster=cluster)
         params = rh.RhsegParams(rh.HsegParams(w, t, MEASURE_OF.get(name, "sqrt-bsmse")), levels, st)
         s = torch.cuda.Stream()
         res = []
