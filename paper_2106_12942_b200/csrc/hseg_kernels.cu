@@ -76,8 +76,9 @@ constexpr int kKB = 16;
 #ifndef RHSEG_DINIT_GRAM
 #define RHSEG_DINIT_GRAM 0  // measured: init 83 -> 88 ms (4x4 blocking turns shared-memory bound) and the loop 376 -> 677 ms (1e-9-wide intervals: 11x more exact pairs); off
 #endif
+constexpr int kDT = 256;  // dinit_dense_kernel's CTA: a 16x16 thread grid over a 64x64 tile
 template <int M, bool IV = false>
-__global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) {
+__global__ void __launch_bounds__(kDT) dinit_dense_kernel(SectionBatch bt) {
     constexpr bool GRAM = IV && RHSEG_DINIT_GRAM;
     const int sec = bt.sec0 + blockIdx.y;
     const int R0 = bt.R0[sec];
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     // bands past B are zero-filled (src-size 0): +0.0 to every accumulator, an identity
     auto stage = [&](int k0, int buf) {
         double* dst = smraw + buf * kStage;
-        for (int e = threadIdx.x; e < 2 * kKB * (kTile / 2); e += kThreads) {
+        for (int e = threadIdx.x; e < 2 * kKB * (kTile / 2); e += kDT) {
             const int op = e / (kKB * (kTile / 2)), r = e % (kKB * (kTile / 2));
             const int kk = r / (kTile / 2), c = r % (kTile / 2);
             const int k = k0 + kk;
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(kThreads) dinit_dense_kernel(SectionBatch bt) 
     }
     if (ti == tj) return;  // diagonal tile already holds both orders (d is bitwise symmetric)
     __syncthreads();
-    for (int e = threadIdx.x; e < kTile * kTile; e += kThreads) {
+    for (int e = threadIdx.x; e < kTile * kTile; e += kDT) {
         const int r = e / kTile, c = e % kTile;  // output row j0+r, column i0+c
         if (j0 + r < R0 && i0 + c < R0) D[(size_t)(j0 + r) * Rp + i0 + c] = sT[c][r];
     }
@@ -250,16 +251,127 @@ __global__ void __launch_bounds__(kThreads) dinit_sparse_kernel(SectionBatch bt)
     }
 }
 
+// APO sections' all-pairs init (IV: fl(a - b) then one DFMA per pair-band, D receives the
+// interval of dinit_dense_kernel<M, true>, bit for bit): 64x64 pair tiles on 128 threads with
+// 8x4 register blocking, so each band step issues 6 shared 16-byte loads per 64 FP64
+// instructions (the 4x4 layout: 4 per 32, and the FP64 pipe sat at 72%).
+#ifndef RHSEG_DINIT_84
+#define RHSEG_DINIT_84 1
+#endif
+constexpr int kDiThreads = 128;
+template <int M>
+__global__ void __launch_bounds__(kDiThreads) dinit_iv84_kernel(SectionBatch bt) {
+    const int sec = bt.sec0 + blockIdx.y;
+    const int R0 = bt.R0[sec];
+    const int nt = (R0 + kTile - 1) / kTile;
+    int t = blockIdx.x;
+    if (t >= nt * (nt + 1) / 2) return;
+    int ti = 0;
+    while (t >= nt - ti) { t -= nt - ti; ++ti; }
+    const int tj = ti + t;
+    const int i0 = ti * kTile, j0 = tj * kTile;
+    const int B = bt.B, Rp = bt.Rp;
+    const double* __restrict__ mu = bt.mu + sec * bt.mu_stride();
+    double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    const uint32_t* __restrict__ cnt = bt.count + (size_t)sec * Rp;
+    constexpr int kStage = 2 * kKB * kTile;
+    __shared__ __align__(16) double smraw[(2 * kStage > kTile * (kTile + 1)) ? 2 * kStage : kTile * (kTile + 1)];
+    double (*sT)[kTile + 1] = reinterpret_cast<double (*)[kTile + 1]>(smraw);
+    // thread (tx, ty): rows i0 + 8 ty + p (p < 8), columns j0 + 4 tx + q (q < 4)
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[8][4];
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
+    auto stage = [&](int k0, int buf) {
+        double* dst = smraw + buf * kStage;
+        for (int e = threadIdx.x; e < 2 * kKB * (kTile / 2); e += kDiThreads) {
+            const int op = e / (kKB * (kTile / 2)), r = e % (kKB * (kTile / 2));
+            const int kk = r / (kTile / 2), c = r % (kTile / 2);
+            const int k = k0 + kk;
+            const double* src = mu + (size_t)min(k, B - 1) * Rp + (op ? j0 : i0) + 2 * c;
+            const uint32_t d = smem_u32(dst + op * kKB * kTile + kk * kTile + 2 * c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(k < B ? 16 : 0)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int nchunk = (B + kKB - 1) / kKB;
+    stage(0, 0);
+    for (int ch = 0; ch < nchunk; ++ch) {
+        if (ch + 1 < nchunk) {
+            stage((ch + 1) * kKB, (ch + 1) & 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        const double (*sA)[kTile] = reinterpret_cast<const double (*)[kTile]>(smraw + (ch & 1) * kStage);
+        const double (*sB)[kTile] = reinterpret_cast<const double (*)[kTile]>(smraw + (ch & 1) * kStage + kKB * kTile);
+#pragma unroll
+        for (int kk = 0; kk < kKB; ++kk) {
+            double a[8], b[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const double2 v = *reinterpret_cast<const double2*>(&sA[kk][8 * ty + 2 * h]);
+                a[2 * h] = v.x;
+                a[2 * h + 1] = v.y;
+            }
+            const double2 b01 = *reinterpret_cast<const double2*>(&sB[kk][4 * tx]);
+            const double2 b23 = *reinterpret_cast<const double2*>(&sB[kk][4 * tx + 2]);
+            b[0] = b01.x; b[1] = b01.y; b[2] = b23.x; b[3] = b23.y;
+#pragma unroll
+            for (int p = 0; p < 8; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double d = __dsub_rn(a[p], b[q]);
+                    acc[p][q] = __fma_rn(d, d, acc[p][q]);
+                }
+        }
+        __syncthreads();
+    }
+    const double rho = 2.0 * (bt.B + 4) * 1.1102230246251565e-16;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const int i = i0 + 8 * ty + p;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int j = j0 + 4 * tx + q;
+            double d = 0.0;
+            if (i < R0 && j < R0) {
+                d = pair_finish<M>((double)cnt[i], (double)cnt[j], acc[p][q], 0.0, 0.0);
+                if (d > 0.0) {
+                    double v;
+                    if (d_pack_interval(__dmul_rd(d, __dsub_rd(1.0, rho)), __dmul_ru(d, __dadd_ru(1.0, rho)), v)) d = v;
+                }
+                D[(size_t)i * Rp + j] = d;
+            }
+            sT[8 * ty + p][4 * tx + q] = d;
+        }
+    }
+    if (ti == tj) return;  // diagonal tile already holds both orders (d is bitwise symmetric)
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTile * kTile; e += kDiThreads) {
+        const int r = e / kTile, c = e % kTile;  // output row j0+r, column i0+c
+        if (j0 + r < R0 && i0 + c < R0) D[(size_t)(j0 + r) * Rp + i0 + c] = sT[c][r];
+    }
+}
+
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st) {
     if (nrun == 0 || R0max == 0) return;
     if (b.spec) {
         const int nt = (R0max + kTile - 1) / kTile;
         dim3 grid(nt * (nt + 1) / 2, nrun);
-        if (b.measure == kSam) dinit_dense_kernel<kSam><<<grid, kThreads, 0, st>>>(b);
-        else if (b.measure == kEuclid && b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kEuclid, true><<<grid, kThreads, 0, st>>>(b);
-        else if (b.measure == kEuclid) dinit_dense_kernel<kEuclid><<<grid, kThreads, 0, st>>>(b);
-        else if (b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kBsmse, true><<<grid, kThreads, 0, st>>>(b);
-        else dinit_dense_kernel<kBsmse><<<grid, kThreads, 0, st>>>(b);
+        if (b.measure == kSam) dinit_dense_kernel<kSam><<<grid, kDT, 0, st>>>(b);
+        else if (b.measure == kEuclid && b.apo && RHSEG_DINIT_FMA && RHSEG_DINIT_84 && !RHSEG_DINIT_GRAM)
+            dinit_iv84_kernel<kEuclid><<<grid, kDiThreads, 0, st>>>(b);
+        else if (b.apo && RHSEG_DINIT_FMA && RHSEG_DINIT_84 && !RHSEG_DINIT_GRAM && b.measure == kBsmse)
+            dinit_iv84_kernel<kBsmse><<<grid, kDiThreads, 0, st>>>(b);
+        else if (b.measure == kEuclid && b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kEuclid, true><<<grid, kDT, 0, st>>>(b);
+        else if (b.measure == kEuclid) dinit_dense_kernel<kEuclid><<<grid, kDT, 0, st>>>(b);
+        else if (b.apo && RHSEG_DINIT_FMA) dinit_dense_kernel<kBsmse, true><<<grid, kDT, 0, st>>>(b);
+        else dinit_dense_kernel<kBsmse><<<grid, kDT, 0, st>>>(b);
     } else {
         dim3 grid((R0max + kThreads - 1) / kThreads, nrun);
         if (b.measure == kSam) dinit_sparse_kernel<kSam><<<grid, kThreads, 0, st>>>(b);

@@ -667,7 +667,7 @@ static int upper_levels(rhseg_ctx* c, const rhseg_params* p, int stop_level, cud
         {
             PhaseTimer t(c, 0, st);
             launch_stitch(ch.sb, ch.cols, pa.sb, pa.cols, ch.map, p->connectivity, st);
-            c->launches += 1;
+            c->launches += 3;  // stitch, pixel assignment, seam links
         }
         CK(cudaGetLastError());
         if (ch.imported) free_level(ch, st);

@@ -15,7 +15,10 @@
 
 namespace rhseg {
 
-constexpr int kThreads = 256;           // CTA size of every section kernel
+#ifndef RHSEG_KTHREADS
+#define RHSEG_KTHREADS 256
+#endif
+constexpr int kThreads = RHSEG_KTHREADS;  // CTA size of every section kernel (the loop's A/B knob)
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxCluster = 16;         // non-portable cluster limit on sm_100a
 constexpr int kNoJ = INT_MAX;           // "no partner" sentinel inside reductions

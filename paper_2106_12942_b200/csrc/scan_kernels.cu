@@ -60,7 +60,7 @@ constexpr int kSKB = 16;  // bands per smem stage
 
 // grid (row tiles covering [row_start,row_stop), column splits). Each CTA folds its
 // column range into per-row (d, j) minima -> part[split][row].
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(256)
 scan_nonadj_kernel(int row_start, int row_stop, int n, int ld, int nb, int W, int cols_per_split,
                    const double* __restrict__ counts, const double* __restrict__ mu,
                    const uint32_t* __restrict__ bits, RowBest* __restrict__ part) {
@@ -82,7 +82,7 @@ scan_nonadj_kernel(int row_start, int row_stop, int n, int ld, int nb, int W, in
             for (int q = 0; q < 4; ++q) acc[p][q] = 0.0;
         for (int k0 = 0; k0 < nb; k0 += kSKB) {
             const int kn = min(kSKB, nb - k0);
-            for (int e = threadIdx.x; e < kSKB * kST; e += kThreads) {
+            for (int e = threadIdx.x; e < kSKB * kST; e += 256) {
                 const int kk = e / kST, r = e % kST;
                 const bool in = kk < kn;
                 sA[kk][r] = (in && i0 + r < n) ? mu[(size_t)(k0 + kk) * ld + i0 + r] : 0.0;
@@ -182,7 +182,7 @@ void launch_scan_nonadjacent(int row_start, int row_stop, int n, int ld, int nb,
     cps = (cps + kST - 1) / kST * kST;
     const int ns = (n + cps - 1) / cps;
     dim3 grid((rows + kST - 1) / kST, ns);
-    scan_nonadj_kernel<<<grid, kThreads, 0, st>>>(row_start, row_stop, n, ld, nb, W, cps, counts, mu, bits,
+    scan_nonadj_kernel<<<grid, 256, 0, st>>>(row_start, row_stop, n, ld, nb, W, cps, counts, mu, bits,
                                                   static_cast<RowBest*>(part));
     scan_combine_kernel<<<(rows + 255) / 256, 256, 0, st>>>(row_start, row_stop, ld, ns,
                                                             static_cast<const RowBest*>(part), out_d, out_j);

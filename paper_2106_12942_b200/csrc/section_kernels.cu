@@ -8,6 +8,8 @@
 //   graph.py:267-281   dense_renumber / label_map_from_graph (first row-major occurrence)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "rhseg_batch.h"
 #include "rhseg_device.cuh"
 
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kThreads)
 stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap, int conn) {
     const int P = blockIdx.x;
     const int pr = P / pcols, pc = P % pcols;
-    const int e = ch.edge, E = pa.edge, B = pa.B;
+    const int B = pa.B;
     __shared__ int scratch[kWarps];
     int cidx[4];
     for (int k = 0; k < 4; ++k) cidx[k] = (2 * pr + (k >> 1)) * ccols + (2 * pc + (k & 1));
@@ -196,17 +198,37 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
         for (int m = threadIdx.x; m < R; m += kThreads)
             pa.nrm2[(size_t)P * pa.Rp + m] = norm2_seq(pmu + m, pa.Rp, B);
     }
-    // 3. parent pixel assignment
+    // 5. union-find links start empty (the inverse list lived here); the parent's pixel
+    //    assignment and the seam links follow as two grid-wide kernels (a level near the
+    //    root has one or four parents of up to 2048^2 pixels: one CTA per parent took
+    //    8.7 ms at C4's root, profiles/r02_ncu_stitch)
+    __syncthreads();
+    for (int i = threadIdx.x; i < pa.Rp; i += kThreads) pparent[i] = -1;
+}
+
+// 3. parent pixel assignment over every pixel of every parent of the level (grid-wide)
+__global__ void __launch_bounds__(kThreads)
+stitch_assign_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, const int* cmap) {
+    const int P = blockIdx.y;
+    const int pr = P / pcols, pc = P % pcols;
+    const int e = ch.edge, E = pa.edge;
     int* passign = pa.assign + (size_t)P * pa.npx;
-    for (int p = threadIdx.x; p < E * E; p += kThreads) {
+    for (int p = blockIdx.x * kThreads + threadIdx.x; p < E * E; p += gridDim.x * kThreads) {
         const int r = p / E, c = p - r * E;
         const int k = (r >= e ? 2 : 0) + (c >= e ? 1 : 0);
+        const int cidx = (2 * pr + (k >> 1)) * ccols + (2 * pc + (k & 1));
         const int lr = r - (k >> 1) * e, lc = c - (k & 1) * e;
-        const int cid = ch.assign[(size_t)cidx[k] * ch.npx + lr * e + lc];
-        passign[p] = cmap[(size_t)cidx[k] * ch.Rp + cid];
+        const int cid = ch.assign[(size_t)cidx * ch.npx + lr * e + lc];
+        passign[p] = cmap[(size_t)cidx * ch.Rp + cid];
     }
-    __syncthreads();
-    // 4. seam links (sections.py:82-100): straight + both diagonals under 8-conn
+}
+
+// 4. seam links (sections.py:82-100): straight + both diagonals under 8-conn; one thread
+//    per seam position r of each parent (grid-wide, atomicOr: order-free)
+__global__ void __launch_bounds__(kThreads) stitch_seam_kernel(SectionBatch ch, SectionBatch pa, int conn) {
+    const int P = blockIdx.y;
+    const int e = ch.edge, E = pa.edge;
+    const int* passign = pa.assign + (size_t)P * pa.npx;
     auto link = [&](int r1, int c1, int r2, int c2) {
         const int a = passign[r1 * E + c1], b = passign[r2 * E + c2];
         if (a == b) return;
@@ -216,29 +238,30 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
             atomicOr(&A[(size_t)b * pa.W + (a >> 5)], 1u << (a & 31));
         }
     };
-    for (int r = threadIdx.x; r < E; r += kThreads) {
-        link(r, e - 1, r, e);
-        if (conn == 8 && r + 1 < E) {
-            link(r, e - 1, r + 1, e);
-            link(r, e, r + 1, e - 1);
-        }
-        link(e - 1, r, e, r);
-        if (conn == 8 && r + 1 < E) {
-            link(e - 1, r, e, r + 1);
-            link(e - 1, r + 1, e, r);
-        }
+    const int r = blockIdx.x * kThreads + threadIdx.x;
+    if (r >= E) return;
+    link(r, e - 1, r, e);
+    if (conn == 8 && r + 1 < E) {
+        link(r, e - 1, r + 1, e);
+        link(r, e, r + 1, e - 1);
     }
-    // 5. union-find links start empty (the inverse list lived here)
-    __syncthreads();
-    for (int i = threadIdx.x; i < pa.Rp; i += kThreads) pparent[i] = -1;
+    link(e - 1, r, e, r);
+    if (conn == 8 && r + 1 < E) {
+        link(e - 1, r, e, r + 1);
+        link(e - 1, r + 1, e, r);
+    }
 }
-
 
 void launch_stitch(const SectionBatch& child, int child_cols, const SectionBatch& parent, int parent_cols,
                    int* child_map, int connectivity, cudaStream_t st) {
     if (parent.nsec == 0) return;
     stitch_kernel<<<parent.nsec, kThreads, 0, st>>>(child, child_cols, parent, parent_cols, child_map,
                                                      connectivity);
+    const int npx = parent.edge * parent.edge;
+    const int bx = std::max(1, std::min((npx + kThreads - 1) / kThreads, (4 * 148 + parent.nsec - 1) / parent.nsec * 4));
+    stitch_assign_kernel<<<dim3(bx, parent.nsec), kThreads, 0, st>>>(child, child_cols, parent, parent_cols, child_map);
+    stitch_seam_kernel<<<dim3((parent.edge + kThreads - 1) / kThreads, parent.nsec), kThreads, 0, st>>>(
+        child, parent, connectivity);
 }
 
 // ---------------------------------------------------------------------------
@@ -278,9 +301,15 @@ void launch_graph_init(const SectionBatch& b, const double* counts, const double
 // ---------------------------------------------------------------------------
 constexpr int kFirstNone = 0x7f7f7f7f;  // memset(0x7f) sentinel
 
+// first occurrence of every label: lanes holding the same label elect the lowest lane
+// (the smallest pixel index of the group) for the one atomicMin -- a root with ~16
+// regions over 4M pixels otherwise serialises on 16 addresses (2.7 ms at C4)
 __global__ void first_occ_kernel(const int* assign, int npx, int* first) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p < npx) atomicMin(&first[assign[p]], p);
+    const bool in = p < npx;
+    const int lab = in ? assign[p] : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, lab);
+    if (in && (threadIdx.x & 31) == __ffs(grp) - 1) atomicMin(&first[lab], p);
 }
 __global__ void rank_kernel(const int* first, int R, int* rank) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
