@@ -158,6 +158,50 @@ __device__ __noinline__ double warp_exact(const double* mi, const double* mj, do
     return pair_finish<M>(ci, cj, s, 0.0, 0.0);
 }
 
+// The same value through a per-warp shared-memory staging row: the lanes write the
+// per-band terms, lane 0 runs the ascending-band sum from shared memory (a shuffle-fed
+// chain stalls every lane of the warp on every one of its B additions), all lanes get
+// the result. stg: B doubles owned by the calling warp.
+template <int M>
+__device__ __noinline__ double warp_exact_stg(const double* mi, const double* mj, double ci, double cj, int B,
+                                              int lane, double* stg) {
+    for (int k0 = 0; k0 < B; k0 += 256) {
+        double term[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 32 * u + lane;
+            const double vi = k < B ? mi[k] : 0.0, vj = k < B ? __ldcg(mj + k) : 0.0;
+            if (M == kSam) {
+                term[u] = __dmul_rn(vi, vj);
+            } else {
+                const double t = __dsub_rn(vi, vj);
+                term[u] = __dmul_rn(t, t);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = k0 + 32 * u + lane;
+            if (k < B) stg[k] = term[u];
+        }
+    }
+    __syncwarp();
+    double s = 0.0;
+    if (lane == 0) {
+        int k = 0;
+        for (; k + 8 <= B; k += 8) {
+            double t[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) t[q] = stg[k + q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s = __dadd_rn(s, t[q]);
+        }
+        for (; k < B; ++k) s = __dadd_rn(s, stg[k]);
+    }
+    s = __shfl_sync(0xffffffffu, s, 0);
+    __syncwarp();  // the staging row may be rewritten by the warp's next call
+    return pair_finish<M>(ci, cj, s, 0.0, 0.0);
+}
+
 // APO: a's best when its single candidate may be an interval (nothing to compare)
 __device__ __forceinline__ void rb_offer_iv(RowBest& b, double v, int j) {
     if (__double_as_longlong(v) < 0) { b.d = v; b.j = j; }

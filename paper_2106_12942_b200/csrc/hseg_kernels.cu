@@ -433,7 +433,7 @@ struct RsSlice {
     double va, vn;
 };
 struct LoopSmem {
-    size_t rsp, livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t xstg, rsp, livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -473,6 +473,7 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
     L.livew = o; o = align16(o + (spec && nstages == 0 ? (size_t)(Rp / 32) * 4 : 0));  // APO: live-region bitset
     L.rsp = o;   o = align16(o + (spec && nstages == 0 ? 2 * kWarps * sizeof(RsSlice) : 0));  // APO: rescan slices
+    L.xstg = o;  o = align16(o + (spec && nstages == 0 ? (size_t)kWarps * B * 8 : 0));  // APO: exact-sum staging rows
     o = (o + 127) & ~size_t(127);
     L.ring = o;
     o += spec && nstages > 0 ? (size_t)nstages * stage_bytes + kThreads * 8 : 0;  // (APO: no ring)
@@ -624,6 +625,14 @@ struct StreamState {
 #ifndef RHSEG_RESCAN_SPLIT
 #define RHSEG_RESCAN_SPLIT 0  // APO: split the walks of a step with few rescans over idle warps (C4 loop 358 -> 376 ms: off)
 #endif
+#ifndef RHSEG_EXACT_STG
+#define RHSEG_EXACT_STG 1  // APO exact sums: lane 0 adds staged terms (0: shuffle-fed chain in every lane)
+#endif
+#if RHSEG_EXACT_STG
+#define RHSEG_WEXACT(...) warp_exact_stg<M>(__VA_ARGS__)
+#else
+#define RHSEG_WEXACT(mi, mj, ci, cj, B, lane, stg) warp_exact<M>(mi, mj, ci, cj, B, lane)
+#endif
 #ifndef RHSEG_KEY32
 #define RHSEG_KEY32 1  // APO rescans on 32-bit keys with redux.sync (0: 64-bit keys, shuffle trees)
 #endif
@@ -704,6 +713,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     unsigned short* ver = reinterpret_cast<unsigned short*>(smem + L.ver);  // APO: region -> mr row
     uint32_t* livew = reinterpret_cast<uint32_t*>(smem + L.livew);          // APO: live regions
     RsSlice* rs_part = reinterpret_cast<RsSlice*>(smem + L.rsp);              // APO: rescan slices
+    double* const xstg = reinterpret_cast<double*>(smem + L.xstg) + (size_t)warp * B;  // APO: this warp's staging row
     double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
@@ -810,7 +820,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     };
     auto exact_pair = [&](int i, int j) {  // whole warp; lane 0 writes D back
         const long long t0 = clock64();
-        const double d = warp_exact<M>(mr + (size_t)ver[i] * B, mr + (size_t)ver[j] * B, (double)cnt[i], (double)cnt[j], B, lane);
+        const double d = RHSEG_WEXACT(mr + (size_t)ver[i] * B, mr + (size_t)ver[j] * B, (double)cnt[i],
+                                           (double)cnt[j], B, lane, xstg);
         if (bt.prof && lane == 0) {
             atomicAdd(bt.prof + 11, 1ull);
             atomicAdd(bt.prof + 12, (unsigned long long)(clock64() - t0));
@@ -2258,7 +2269,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 for (int t = warp; t < n1; t += kWarps) {
                     const int e = l1[t], j = e & 0x3fff, r = j - lo;
                     const bool aj = !(e & 0x4000);
-                    const double daj = warp_exact<M>(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane);
+                    const double daj = RHSEG_WEXACT(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane, xstg);
                     const int bj = aj ? bAj[r] : bNj[r];
                     double db = aj ? bAd[r] : bNd[r];
                     const bool binterval = bj >= 0 && d_is_interval(db);
@@ -2321,7 +2332,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                             else rb_offer_iv(pN, v, j);
                         }
                     } else {
-                        const double d = warp_exact<M>(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane);
+                        const double d = RHSEG_WEXACT(mua, mr + (size_t)ver[j] * B, nn, (double)cnt[j], B, lane, xstg);
                         if (lane == 0) {
                             D[(size_t)j * Rp + a] = d;
                             D[(size_t)a * Rp + j] = d;

@@ -35,28 +35,25 @@ leaf_init_kernel(SectionBatch bt, const float* __restrict__ cube, int N, int col
         parent[p] = -1;
         if (p < R0) assign[p] = p;
     }
-    // mu[k][p] (band-major; coalesced along the section row of each band plane)
-    for (int idx = threadIdx.x; idx < B * R0; idx += kThreads) {
-        const int k = idx / R0, p = idx - k * R0;
-        const int r = p / e, c = p - r * e;
-        mu[(size_t)k * Rp + p] = (double)cube[((size_t)k * N + orow + r) * N + ocol + c];
-    }
-    // sums[c][p][k] (region-major): transpose 32x32 tiles through smem
+    // one read of the window: 32 pixels x 32 bands tiles, coalesced along the pixels;
+    // mu[k][p] (band-major) is written straight from the loads, sums[c][p][k]
+    // (region-major) through a shared-memory transpose
     __shared__ double tile[32][33];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x kWarps
     for (int p0 = 0; p0 < R0; p0 += 32)
         for (int k0 = 0; k0 < B; k0 += 32) {
-            for (int kk = ty; kk < 32; kk += 8) {
+            for (int kk = ty; kk < 32; kk += kWarps) {
                 const int p = p0 + tx, k = k0 + kk;
                 double v = 0.0;
                 if (p < R0 && k < B) {
                     const int r = p / e, c = p - r * e;
                     v = (double)cube[((size_t)k * N + orow + r) * N + ocol + c];
+                    mu[(size_t)k * Rp + p] = v;
                 }
                 tile[kk][tx] = v;
             }
             __syncthreads();
-            for (int pp = ty; pp < 32; pp += 8) {
+            for (int pp = ty; pp < 32; pp += kWarps) {
                 const int p = p0 + pp, k = k0 + tx;
                 if (p < R0 && k < B)
                     for (int cc = 0; cc < bt.C; ++cc)
