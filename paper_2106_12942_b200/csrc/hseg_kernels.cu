@@ -633,6 +633,9 @@ struct StreamState {
 #else
 #define RHSEG_WEXACT(mi, mj, ci, cj, B, lane, stg) warp_exact<M>(mi, mj, ci, cj, B, lane)
 #endif
+#ifndef RHSEG_AROW_REGS
+#define RHSEG_AROW_REGS 0  // APO rescans: the row's adjacency words in registers, shuffled per word (C4 loop 343 -> 418 ms: off)
+#endif
 #ifndef RHSEG_KEY32
 #define RHSEG_KEY32 1  // APO rescans on 32-bit keys with redux.sync (0: 64-bit keys, shuffle trees)
 #endif
@@ -969,6 +972,21 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         double va = kInf, vn = kInf;
         int km = 0;  // widest interval code over both stages (only widens the test)
         constexpr int U = RHSEG_RESCAN_U;
+        // the row's adjacency words (W <= 64 on APO sections), one or two per lane, loaded
+        // once: every walk iteration then waits on its D loads only, not on a global
+        // adjacency load in front of them (the merges rewrite these rows, so L1 rarely
+        // holds them)
+        uint32_t awl0 = 0u, awl1 = 0u;
+        const bool areg = RHSEG_AROW_REGS && W <= 64;  // (uniform)
+        if (areg) {
+            awl0 = lane < W ? arow[lane] : 0u;
+            awl1 = 32 + lane < W ? arow[32 + lane] : 0u;
+        }
+        auto aword = [&](int w) -> uint32_t {  // word w of the row (w uniform or per lane)
+            if (!areg) return arow[w];
+            const uint32_t x0 = __shfl_sync(0xffffffffu, awl0, w & 31), x1 = __shfl_sync(0xffffffffu, awl1, w & 31);
+            return w < 32 ? x0 : x1;
+        };
         // the walk is specialised on the stage mask: a single-stage rescan (the common
         // case) tracks one pair of keys
         auto walk = [&](auto MKC) {
@@ -999,9 +1017,10 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     for (int u = 0; u < U; ++u) {
                         const int sl = s0 + 32 * u + lane;
                         const int j = sl < shi ? col[sl] : -1;
+                        const uint32_t awj = aword(j >= 0 ? j >> 5 : 0);  // (every lane: shuffles)
                         bool c = false, aj = false;
                         if (j >= 0 && j != i && j != ex && j != rs_exb && ((livew[j >> 5] >> (j & 31)) & 1u)) {
-                            aj = (arow[j >> 5] >> (j & 31)) & 1u;
+                            aj = (awj >> (j & 31)) & 1u;
                             c = aj ? (MK & 1) : (MK & 2);
                         }
                         jv[u] = j;
@@ -1020,7 +1039,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int w = w0 + u;
-                        const uint32_t lw = w < whi ? livew[w] : 0u, aw = w < whi ? arow[w] : 0u;
+                        const uint32_t lw = w < whi ? livew[w] : 0u, aw = w < whi ? aword(w) : 0u;
                         const int j = (w << 5) + lane;
                         const bool aj = (aw >> lane) & 1u;
                         const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (MK & 1) : (MK & 2));
