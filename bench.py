@@ -475,9 +475,10 @@ def roofline(name, edge, bands, levels, w, phases, handle, leaf=None):
     flops = nleaf * (R0 * (R0 + 1) // 2) * (3 * bands + 5) if w > 0 else 0
     ach = flops / (dinit_ms * 1e-3) / 1e12 if dinit_ms > 0 else 0.0
     peak = fma.value / 1e12
-    dinit = {"kernel": "dinit_dense_kernel (all-pairs fp64 dissimilarity)" if w > 0 else "dinit_sparse_kernel",
+    dname = "dinit_sparse_kernel" if w <= 0 else ("dinit_iv84_kernel" if var in (2, 3) else "dinit_dense_kernel")
+    dinit = {"kernel": dname + " (all-pairs fp64 dissimilarity)",
              "bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-             "frac": ach / peak if peak else None, "traffic": ncu_traffic(name, "dinit_dense_kernel"),
+             "frac": ach / peak if peak else None, "traffic": ncu_traffic(name, dname),
              "kernel_ms": dinit_ms, "algorithmic_flops": flops,
              "algorithmic_model": "leaf pairs R0(R0+1)/2 x (3B+5) flops (sub, mul, add per band + finish)",
              "peak_source": "measured live: rhseg_fp64_fma_peak (DFMA loop, 2 flops/instr)"}
