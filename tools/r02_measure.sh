@@ -2,7 +2,7 @@
 # Round-2 measurement pass: every workload's device time, the C4 bench line, the ncu
 # launch list of the bench command, one full ncu capture of the leaf-level loop and of
 # the all-pairs init (C4), DRAM bytes per kernel, and the GPU suite.
-O=gpurun_out/r02/measure
+O=gpurun_out/r02/final
 mkdir -p $O
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; rc=$?; echo "smoke rc=$rc"
 [ $rc -ne 0 ] && exit 1
@@ -11,8 +11,8 @@ RHSEG_PROFILE=1 timeout 300 python tools/profile_loop.py c4 c2 c5w0 c5w1 > $O/pr
 timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench_c4.json 2> $O/bench_c4.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c4.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_bench.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__inst_executed_pipe_fp64.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum --clock-control none --csv -k regex:"hseg_loop|hseg_adj|dinit_dense" -c 3 --log-file $O/traffic_c4.csv python tools/c4_paths.py dev 1 > $O/ncu_traffic.log 2>&1; echo "ncu traffic rc=$?"
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,sm__inst_executed_pipe_fp64.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum --clock-control none --csv -k regex:"hseg_loop|hseg_adj|dinit_dense|dinit_iv84" -c 3 --log-file $O/traffic_c4.csv python tools/c4_paths.py dev 1 > $O/ncu_traffic.log 2>&1; echo "ncu traffic rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"hseg_loop_kernel" -c 1 -f -o $O/loop_c4 python tools/c4_paths.py dev 1 > $O/ncu_loop.log 2>&1; echo "ncu loop rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"dinit_dense" -c 1 -f -o $O/dinit_c4 python tools/c4_paths.py dev 1 > $O/ncu_dinit.log 2>&1; echo "ncu dinit rc=$?"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"dinit_iv84" -c 1 -f -o $O/dinit_c4 python tools/c4_paths.py dev 1 > $O/ncu_dinit.log 2>&1; echo "ncu dinit rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"hseg_adj_kernel" -c 1 -f -o $O/adj_c5w0 python tools/profile_loop.py c5w0 > $O/ncu_adj.log 2>&1; echo "ncu adj rc=$?"
 timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "gpu suite rc=$?"
