@@ -452,7 +452,6 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.misc = o;  o += 64;
     L.rpart = o; o += 2 * sizeof(RowBest);
     L.bars = o;  o += kMaxStages * 8;  // full[nstages]
-    L.mua = o;   o = align16(o + (size_t)B * 8);
     L.bAd = o;   o = align16(o + Rs * 8);
     L.bNd = o;   o = align16(o + Rs * 8);
     L.bAj = o;   o = align16(o + Rs * 4);
@@ -473,6 +472,8 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
     L.livew = o; o = align16(o + (spec && nstages == 0 ? (size_t)(Rp / 32) * 4 : 0));  // APO: live-region bitset
     L.rsp = o;   o = align16(o + (spec && nstages == 0 ? 2 * kWarps * sizeof(RsSlice) : 0));  // APO: rescan slices
+    // the band-sized arrays last: with a compile-time capacity every offset above folds
+    L.mua = o;   o = align16(o + (size_t)B * 8);
     L.xstg = o;  o = align16(o + (spec && nstages == 0 ? (size_t)kWarps * B * 8 : 0));  // APO: exact-sum staging rows
     o = (o + 127) & ~size_t(127);
     L.ring = o;
@@ -636,6 +637,9 @@ struct StreamState {
 #ifndef RHSEG_AROW_REGS
 #define RHSEG_AROW_REGS 0  // APO rescans: the row's adjacency words in registers, shuffled per word (C4 loop 343 -> 418 ms: off)
 #endif
+#ifndef RHSEG_RPC
+#define RHSEG_RPC 1  // APO loop instantiated for compile-time capacities 1024 and 64
+#endif
 #ifndef RHSEG_KEY32
 #define RHSEG_KEY32 1  // APO rescans on 32-bit keys with redux.sync (0: 64-bit keys, shuffle trees)
 #endif
@@ -645,7 +649,11 @@ struct StreamState {
 #ifndef RHSEG_APO_MINBLOCKS
 #define RHSEG_APO_MINBLOCKS 2
 #endif
-template <bool CLUSTER, bool SPEC, int M, bool APO = false>
+// RPC: the padded capacity as a compile-time constant (0 = bt.Rp at run time). The APO
+// loop is instantiated for the capacities of the BASELINE levels (1024: 32x32 leaves, 64:
+// every level above at t=16), so the shared-memory layout and the D / sums / adjacency
+// strides fold to constants instead of being recomputed under register pressure.
+template <bool CLUSTER, bool SPEC, int M, bool APO = false, int RPC = 0>
 __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MINBLOCKS) hseg_loop_kernel(SectionBatch bt) {
     extern __shared__ __align__(128) unsigned char smem[];
     const long long t_entry = clock64();
@@ -654,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     const int sec = bt.sec0 + (int)(blockIdx.x / C);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int R0 = bt.R0[sec];
-    const int B = bt.B, Rp = bt.Rp, W = bt.W;
+    const int B = bt.B, Rp = RPC ? RPC : bt.Rp, W = RPC ? RPC / 32 : bt.W;
     const int target = bt.target[sec];
     const int Rs = own_rows(R0, C);
     const int lo = min(R0, rank * Rs), hi = min(R0, lo + Rs);
@@ -671,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     constexpr int ES = (int)sizeof(SE);
     const int SB = bt.stage_bytes;  // ring stage size and depth chosen by the host
     const int NS = bt.nstages;      // (deeper ring when the level has <= 1 CTA per SM)
-    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, SB, NS);
+    const LoopSmem L = loop_smem_layout(Rp, C, B, SPEC, TOP2, APO ? 0 : SB, APO ? 0 : NS);
     Slot* slot = reinterpret_cast<Slot*>(smem + L.slot);
     Slot* rslot = reinterpret_cast<Slot*>(smem + L.rslot);
     Pair* pscr = reinterpret_cast<Pair*>(smem + L.pscr);
@@ -704,23 +712,24 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     int& nnb = misc[13];
     double* ring = reinterpret_cast<double*>(smem + L.ring);
 
-    double* const mu0 = bt.mu + sec * bt.mu_stride();
-    double* const mu1 = STREAM ? bt.mu2 + sec * bt.mu_stride() : nullptr;
+    const size_t mus = (size_t)B * Rp;  // (bt.mu_stride() with the folded capacity)
+    double* const mu0 = bt.mu + sec * mus;
+    double* const mu1 = STREAM ? bt.mu2 + sec * mus : nullptr;
     SE* const sb0 = mu0;  // the streamed mean buffers (ping-pong)
     SE* const sb1 = mu1;
     // APO: region-major copy of the exact cached means [Rp][B] (in the mu2 allocation)
     // APO: versioned region-major means [2 Rp][B] (row i: initial mean of region i; row
     // R0 + t: the mean created by step t) -- the exact re-evaluations read them, and
     // the log's exact values are computed after the loop from (old a, b) versions
-    double* const mr = APO ? bt.mu2 + 2 * sec * bt.mu_stride() : nullptr;
+    double* const mr = APO ? bt.mu2 + 2 * sec * mus : nullptr;
     unsigned short* ver = reinterpret_cast<unsigned short*>(smem + L.ver);  // APO: region -> mr row
     uint32_t* livew = reinterpret_cast<uint32_t*>(smem + L.livew);          // APO: live regions
     RsSlice* rs_part = reinterpret_cast<RsSlice*>(smem + L.rsp);              // APO: rescan slices
     double* const xstg = reinterpret_cast<double*>(smem + L.xstg) + (size_t)warp * B;  // APO: this warp's staging row
-    double* __restrict__ D = bt.D + (sec - bt.sec0) * bt.d_stride();
+    double* __restrict__ D = bt.D + (size_t)(sec - bt.sec0) * ((size_t)Rp * Rp);
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
-    double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * bt.sums_copy();
-    uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * bt.adj_copy();
+    double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * ((size_t)Rp * B);
+    uint32_t* __restrict__ adj = bt.adj + ((size_t)sec * C + rank) * ((size_t)Rp * W);
 
     // Rescan of one owned row from D (mask bit0: adjacent stage, bit1: non-adjacent
     // stage) -- the full-row search of _kernels.py restricted to rows whose cached
@@ -2507,10 +2516,16 @@ int launch_hseg_loop(const SectionBatch& b, int nrun, cudaStream_t st) {
         RHSEG_PICK(kSam)
     } else if (b.measure == kEuclid) {
         RHSEG_PICK(kEuclid)
-        if (b.apo) kern = hseg_loop_kernel<false, true, kEuclid, true>;
+        if (b.apo)
+            kern = (RHSEG_RPC && b.Rp == 1024) ? hseg_loop_kernel<false, true, kEuclid, true, 1024>
+                   : (RHSEG_RPC && b.Rp == 64) ? hseg_loop_kernel<false, true, kEuclid, true, 64>
+                                               : hseg_loop_kernel<false, true, kEuclid, true>;
     } else {
         RHSEG_PICK(kBsmse)
-        if (b.apo) kern = hseg_loop_kernel<false, true, kBsmse, true>;
+        if (b.apo)
+            kern = (RHSEG_RPC && b.Rp == 1024) ? hseg_loop_kernel<false, true, kBsmse, true, 1024>
+                   : (RHSEG_RPC && b.Rp == 64) ? hseg_loop_kernel<false, true, kBsmse, true, 64>
+                                               : hseg_loop_kernel<false, true, kBsmse, true>;
     }
     if (b.apo && !apo_capable(b.spec != 0, b.C, b.measure)) return cudaErrorInvalidValue;
 #undef RHSEG_PICK
