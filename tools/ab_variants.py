@@ -15,13 +15,13 @@ CHILD = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, ROOT)
 import paper_2106_12942_b200 as rh
-from bench import WORKLOADS, _phase_ms_of
+from bench import MEASURE_OF, WORKLOADS, _phase_ms_of
 spec, crop, levels, w, t, st = WORKLOADS[NAME]
 cube_h = np.load(CUBE, mmap_mode='r')
 cube = torch.from_numpy(np.ascontiguousarray(cube_h)).cuda()
 bands, edge, _ = cube.shape
 ex = rh.B200Executor(device=0)
-params = rh.RhsegParams(rh.HsegParams(w, t), levels, st)
+params = rh.RhsegParams(rh.HsegParams(w, t, MEASURE_OF.get(NAME, 'sqrt-bsmse')), levels, st)
 s = torch.cuda.Stream()
 res = []
 with torch.cuda.stream(s):
