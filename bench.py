@@ -454,15 +454,17 @@ def roofline(name, edge, bands, levels, w, phases, handle, leaf=None):
         per_sec = sum(4 * R * 8 + 4 * bands * 8 for R in steps) + resc_per_sec * rbar * 8
         note = ("APO loop: sum_steps (4R*8 + 4B*8) + rescans*mean(R)*8 bytes; %.0f rescans per leaf "
                 "(latency-bound step chain, not a stream)" % resc_per_sec)
-    elif var == 1:
+    elif var in (1, 4):
         per_sec = sum(R * (8 * bands + 16) for R in steps)
-        note = "mean-stream loop: the live regions' fp64 means once per step, sum_steps R_live*(8B+16)"
+        note = ("mean-stream loop" if var == 1 else "grid loop (one section on a group of CTAs)") + \
+            ": the live regions' fp64 means once per step, sum_steps R_live*(8B+16)"
     else:
         per_sec = (R0 - t) * 10 * 8 * bands
         note = "w=0 loop: ~10 band-sum rows of 8B bytes per step (latency-bound, not a stream)"
     algo = nleaf * per_sec
     achieved = algo / (loop_ms * 1e-3) / 1e9 if loop_ms > 0 else 0.0
-    kname = {3: "hseg_apo_kernel", 0: "hseg_adj_kernel"}.get(var, "hseg_loop_kernel") if leaf["cluster"] == 1 \
+    kname = "hseg_grid_kernel" if var == 4 else \
+        {3: "hseg_apo_kernel", 0: "hseg_adj_kernel"}.get(var, "hseg_loop_kernel") if leaf["cluster"] == 1 \
         else "hseg_loop_kernel"
     loop = {"kernel": kname + " (persistent per-section merge loop)",
             "loop_variant": leaf["loop"], "ctas_per_section": leaf["cluster"],

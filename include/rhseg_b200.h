@@ -43,7 +43,7 @@ extern "C" {
 #define RHSEG_E_INVALID 1     /* ValueError in the reference (engine.py:37-42, recursive.py:41-47) */
 #define RHSEG_E_INDIVISIBLE 2 /* errors.IndivisibleImage (sections.py:61-65) */
 #define RHSEG_E_CUDA 3        /* CUDA failure / no sm_100a device */
-#define RHSEG_E_TOO_LARGE 4   /* section exceeds the device limits (R0 > 16384 regions) */
+#define RHSEG_E_TOO_LARGE 4   /* a section's dissimilarity matrix (R0^2 fp64) exceeds device memory */
 #define RHSEG_E_STATE 5       /* no result available / wrong call order */
 #define RHSEG_E_TOO_MANY_LABELS 6 /* errors.TooManyLabels: label above 65535 in a PGM (hsio.py:85-101) */
 #define RHSEG_E_IO 7          /* OSError: an output file cannot be opened or written */
@@ -195,6 +195,7 @@ int rhseg_result_rescans(rhseg_ctx *ctx, int32_t level, int64_t *n);
 #define RHSEG_LOOP_STREAM 1
 #define RHSEG_LOOP_APO 2
 #define RHSEG_LOOP_APO_RECUT 3
+#define RHSEG_LOOP_GRID 4 /* grid_loop.cu: sections above a cluster's capacity (cluster = CTAs per section) */
 int rhseg_result_level_info(rhseg_ctx *ctx, int32_t level, int32_t *nsec, int32_t *rp, int32_t *cluster,
                             int32_t *loop_variant, int64_t *merges);
 /* FP64 DADD/DMUL issue-rate probe: returns achieved fp64 ops/s of a pure

@@ -206,7 +206,7 @@ def make_params(weight, target, section_target, levels, connectivity=8, measure=
     return p
 
 
-LOOP_NAMES = {0: "adjacent (w=0)", 1: "mean stream", 2: "APO", 3: "APO re-cut"}
+LOOP_NAMES = {0: "adjacent (w=0)", 1: "mean stream", 2: "APO", 3: "APO re-cut", 4: "grid"}
 
 
 def level_info(handle, level: int) -> dict:

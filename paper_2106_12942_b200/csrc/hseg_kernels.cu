@@ -411,6 +411,10 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #ifndef RHSEG_RESCAN_PREFETCH
 #define RHSEG_RESCAN_PREFETCH 1
 #endif
+#ifndef RHSEG_RESCAN_STAGE
+#define RHSEG_RESCAN_STAGE 0  // APO: first N rescans' D rows bulk-copied to shared memory (C4 loop 319 -> 354/357/367 ms for N = 1/2/3: off)
+#endif
+constexpr int kRsStage = RHSEG_RESCAN_STAGE;
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -433,7 +437,7 @@ struct RsSlice {
     double va, vn;
 };
 struct LoopSmem {
-    size_t xstg, rsp, livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
+    size_t xstg, rbuf, rsp, livew, ver, apk, sdv, slot, rslot, pscr, rscr, spart, misc, rpart, bars, mua, bAd, bNd, bAj, bNj, inv, cnt, col, slot_of, bAd2, bNd2,
         bAj2, bNj2, cx, nbl, sra, ring, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -472,6 +476,8 @@ __host__ __device__ inline LoopSmem loop_smem_layout(int Rp, int C, int B, bool 
     L.ver = o;   o = align16(o + (spec && nstages == 0 ? (size_t)Rp * 2 : 0));  // APO: mean version per region
     L.livew = o; o = align16(o + (spec && nstages == 0 ? (size_t)(Rp / 32) * 4 : 0));  // APO: live-region bitset
     L.rsp = o;   o = align16(o + (spec && nstages == 0 ? 2 * kWarps * sizeof(RsSlice) : 0));  // APO: rescan slices
+    o = (o + 127) & ~size_t(127);
+    L.rbuf = o;  o += spec && nstages == 0 ? (size_t)kRsStage * Rp * 8 : 0;  // APO: staged D rows of rescans
     // the band-sized arrays last: with a compile-time capacity every offset above folds
     L.mua = o;   o = align16(o + (size_t)B * 8);
     L.xstg = o;  o = align16(o + (spec && nstages == 0 ? (size_t)kWarps * B * 8 : 0));  // APO: exact-sum staging rows
@@ -726,6 +732,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     uint32_t* livew = reinterpret_cast<uint32_t*>(smem + L.livew);          // APO: live regions
     RsSlice* rs_part = reinterpret_cast<RsSlice*>(smem + L.rsp);              // APO: rescan slices
     double* const xstg = reinterpret_cast<double*>(smem + L.xstg) + (size_t)warp * B;  // APO: this warp's staging row
+    double* const rbuf = reinterpret_cast<double*>(smem + L.rbuf);  // APO: staged D rows of the first rescans
+    uint32_t rbph = 0u;  // (uniform) parity each staged-row barrier completes next
     double* __restrict__ D = bt.D + (size_t)(sec - bt.sec0) * ((size_t)Rp * Rp);
     double* __restrict__ n2g = M == kSam ? bt.nrm2 + (size_t)sec * Rp : nullptr;
     double* __restrict__ sums = bt.sums + ((size_t)sec * C + rank) * ((size_t)Rp * B);
@@ -973,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     // part / nparts: this warp walks one slice of the row (nparts > 1: idle warps share the
     // rescans of a step with few of them; the slice's keys go to rs_part[item] and
     // rescanf_finish combines them after the post-rescan barrier)
-    auto rescanf = [&](int i, int mask, int ex, int part, int nparts, int item) {
+    auto rescanf = [&](int i, int mask, int ex, int part, int nparts, int item, const double* sbuf = nullptr) {
         const uint32_t* arow = adj + (size_t)i * W;
         const double* drow = D + (size_t)i * Rp;
         unsigned a1 = ~0u, a2 = ~0u, n1 = ~0u, n2 = ~0u;
@@ -1034,7 +1042,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         }
                         jv[u] = j;
                         sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                        dv[u] = c ? (sbuf ? sbuf[j] : __ldcs(drow + j)) : 0.0;
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) take(dv[u], jv[u], sel[u] & 1u, sel[u] & 2u);
@@ -1053,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         const bool aj = (aw >> lane) & 1u;
                         const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (MK & 1) : (MK & 2));
                         sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                        dv[u] = c ? __ldcs(drow + j) : 0.0;
+                        dv[u] = c ? (sbuf ? sbuf[j] : __ldcs(drow + j)) : 0.0;
                     }
                 };
                 if (RHSEG_RESCAN_PIPE) {
@@ -1085,6 +1093,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             else if (mask == 2) walk(std::integral_constant<int, 2>{});
             else walk(std::integral_constant<int, 3>{});
         }
+        if (kRsStage && sbuf) fence_proxy_async_shared();  // the buffer's next fill is an async write
         km = __reduce_max_sync(0xffffffffu, km);
         // warp minimum of one stage: the smallest key, the second smallest (== the
         // smallest on a tie), the winner's column and D value
@@ -1566,6 +1575,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             for (int s = 0; s < NS; ++s) {
                 mbar_init(&bars[s], 1);
             }
+        if (APO && kRsStage && tid == 0)
+            for (int s = 0; s < kRsStage; ++s) mbar_init(&bars[s], 1);
         mbar_init_fence();
     }
     if (tid == 0) {
@@ -1899,9 +1910,23 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         // the rescans (which skip a and b and read nothing the merge writes but bits a
         // and b of neighbour rows' adjacency words); the others merge with every thread
         constexpr int MT = APO ? 2 * 32 : kThreads;  // merging threads
+        uint32_t rbph_now = 0u;
         if (APO) {
             __syncthreads();  // the invalidated-row list is complete
             rs_exb = b;
+            if (kRsStage) {
+                // the first kRsStage listed rows: one bulk copy of the D row into shared
+                // memory each (issued by warp 2, which then starts the rescans too)
+                const int nst = min(ninv, kRsStage);
+                rbph_now = rbph;
+                rbph ^= (1u << nst) - 1u;
+                if (warp == 2 && lane < nst) {
+                    const int i = inv[lane] >> 2;
+                    const uint32_t bytes = (uint32_t)(((R0 + 1) & ~1) * 8);
+                    mbar_arrive_expect_tx(&bars[lane], bytes);
+                    bulk_g2s(rbuf + (size_t)lane * Rp, D + (size_t)i * Rp, bytes, &bars[lane]);
+                }
+            }
         }
         uint32_t* ra = adj + (size_t)a * W;
         if (!APO || warp < 2) {
@@ -1969,7 +1994,12 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 if (lane == 0) k = atomicAdd(&misc[12], 1);
                 k = __shfl_sync(0xffffffffu, k, 0);
                 if (k >= ni) break;
-                rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0);
+                if (kRsStage && k < kRsStage) {
+                    mbar_wait(&bars[k], (rbph_now >> k) & 1u);
+                    rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0, rbuf + (size_t)k * Rp);
+                } else {
+                    rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0);
+                }
                 ++nr;
             }
             if (bt.prof && lane == 0 && nr) {
@@ -2409,6 +2439,9 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                                        nullptr, pA, pN, inv, &ninv);
             }
         }
+        // staged rescans bulk-copy D rows (async proxy) that this step's column a' writes
+        // (generic proxy) feed: order them before the next step's copies
+        if (APO && kRsStage) fence_proxy_async_global();
         if (SPEC) block_min_rb2(pA, pN, rscr);
         else pA = block_min_rb(pA, rscr);
         if (APO) {  // a's new mean becomes version R0 + step (the old one stays for the log)

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -112,8 +113,10 @@ int set_error(int code, const char* msg) { return fail(code, msg); }
     } while (0)
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
-// Largest section the merge loop supports: region ids are stored as 14-bit fields in
-// the loop kernel's shared-memory lists and keys (hseg_kernels.cu).
+// Largest section the shared-memory loops hold (one CTA, or a cluster of up to 16 CTAs;
+// 14-bit region ids in the loop kernel's lists and keys, hseg_kernels.cu). Larger sections
+// run on the grid loop (grid_loop.cu), limited only by D's R^2 fp64 in HBM
+// (rhseg_ctx::max_regions).
 constexpr long long kMaxSectionRegions = 16384;
 
 #ifndef RHSEG_L2_PERSIST_MB
@@ -129,6 +132,8 @@ struct Level {
     int level = 0, rows = 0, cols = 0, row0 = 0, col0 = 0, nsec = 0, edge = 0, Rp = 0, W = 0, C = 1, B = 0,
         R0max = 0;
     bool imported = false;  // state received from other ranks: not part of this ctx's logs
+    bool grid = false;      // merge loop on a group of co-resident CTAs (grid_loop.cu)
+    int gridG = 0;          // CTAs per section of the grid loop's last launch
     int measure = 0;        // 0 sqrt-bsmse, 1 euclidean, 2 sam
     std::vector<int> R0h, tgth, nlogh, convh;
     std::vector<long long> pairsh, rescsh;
@@ -143,6 +148,7 @@ struct Level {
 struct rhseg_ctx {
     int device = 0;
     int nsm = 148;
+    long long max_regions = kMaxSectionRegions;  // largest section D fits (set from the HBM size)
     cudaStream_t stream = nullptr;
     std::vector<Level> levels;  // processing order == log order (L .. 1)
     bool have = false;
@@ -246,12 +252,23 @@ static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced, b
 }
 
 // Allocate and zero one level's device state. R0h/tgth must be filled.
+// Grid loop selection: RHSEG_GRID=1 runs every multi-CTA (cluster) section on the grid
+// loop, RHSEG_GRID=0 only the sections a cluster cannot hold.
+static int grid_env() {
+    static const int v = [] {
+        const char* e = getenv("RHSEG_GRID");
+        return e && *e ? atoi(e) : -1;
+    }();
+    return v;
+}
+
 static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, int forced_C, int slot) {
     lv.R0max = 0;
     for (int r : lv.R0h) lv.R0max = std::max(lv.R0max, r);
-    if (lv.R0max > kMaxSectionRegions)
-        return fail(RHSEG_E_TOO_LARGE, "section with " + std::to_string(lv.R0max) + " regions exceeds " +
-                                           std::to_string(kMaxSectionRegions));
+    if (lv.R0max > c->max_regions)
+        return fail(RHSEG_E_TOO_LARGE, "section with " + std::to_string(lv.R0max) + " regions: its " +
+                                           "dissimilarity matrix exceeds device memory (max " +
+                                           std::to_string(c->max_regions) + " regions)");
     lv.Rp = std::max(64, (lv.R0max + 63) / 64 * 64);
     lv.W = lv.Rp / 32;
     const bool spec = weight > 0.0;
@@ -266,9 +283,11 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
                    220 * 1024 &&
                (lv.Rp + C - 1) / C <= hseg_loop_max_rows();
     };
-    // grow the cluster until the per-CTA row slice fits shared memory
+    // grow the cluster until the per-CTA row slice fits shared memory; sections no
+    // cluster holds (or every cluster section under RHSEG_GRID=1) run on the grid loop
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
-    if (!fits(lv.C)) return fail(RHSEG_E_TOO_LARGE, "section state exceeds shared memory");
+    lv.grid = !fits(lv.C) || lv.R0max > kMaxSectionRegions || (grid_env() == 1 && lv.C > 1);
+    if (lv.grid) lv.C = 1;
     // stream ring geometry (runtime knobs). Deeper (4 x 32 KB) or bigger (2 x 96 KB)
     // rings for levels with at most one CTA per SM were both measured slower on C2
     // (47 -> 87 / 82 ms): the shared-memory carveout takes the L1 that the
@@ -277,9 +296,9 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     // bounded from D rows a and b: no stream ring; the second mean buffer holds the
     // region-major means the exact re-evaluations read
     const char* apo_env = getenv("RHSEG_APO");
-    const bool apo = hseg_apo_capable(spec, lv.C, lv.measure) && !(apo_env && apo_env[0] == '0');
+    const bool apo = !lv.grid && hseg_apo_capable(spec, lv.C, lv.measure) && !(apo_env && apo_env[0] == '0');
     const int stage_bytes = hseg_loop_stage_bytes(spec, lv.C, lv.measure);
-    const int nstages = apo ? 0 : hseg_loop_default_stages();
+    const int nstages = (apo || lv.grid) ? 0 : hseg_loop_default_stages();
     const size_t ns = (size_t)lv.nsec, Rp = (size_t)lv.Rp, B = (size_t)lv.B, W = (size_t)lv.W,
                  C = (size_t)lv.C, npx = (size_t)lv.edge * lv.edge;
     // keep block
@@ -303,10 +322,11 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     const size_t oAdj = take(ns * C * Rp * W * 4);
     lv.work_zero = o;
     // w = 0 (adj_loop.cu, one CTA per section) keeps region-major means in mu2
-    const bool adjl = !spec && lv.C == 1;
+    const bool adjl = !spec && lv.C == 1 && !lv.grid;
     const size_t oMu = take(ns * B * Rp * 8),
-                 oMu2 = take(spec ? (apo ? 2 : 1) * ns * B * Rp * 8 : (adjl ? ns * B * Rp * 8 : 0)),  // APO: versioned means
+                 oMu2 = take(lv.grid ? 0 : spec ? (apo ? 2 : 1) * ns * B * Rp * 8 : (adjl ? ns * B * Rp * 8 : 0)),  // APO: versioned means
                  oRec = take(apo ? ns * Rp * 16 : 0),
+                 oGs = take(lv.grid ? ns * grid_loop_scratch_bytes(c->nsm, lv.B, lv.W) : 0),
                  oSums = take(ns * C * Rp * B * 8);
     const size_t work_bytes = o;
     {
@@ -357,7 +377,12 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     b.nresc = reinterpret_cast<long long*>(K + oRs);
     b.adj = reinterpret_cast<uint32_t*>(Wk + oAdj);
     b.mu = reinterpret_cast<double*>(Wk + oMu);
-    b.mu2 = (spec || adjl) ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.mu2 = (!lv.grid && (spec || adjl)) ? reinterpret_cast<double*>(Wk + oMu2) : nullptr;
+    b.gscr = lv.grid ? reinterpret_cast<void*>(Wk + oGs) : nullptr;
+    if (lv.grid) {
+        const char* e = getenv("RHSEG_GRID_CTAS");  // cap on CTAs per section (experiments)
+        b.G = e && *e ? std::max(0, atoi(e)) : 0;
+    }
     b.apo_rec = apo ? reinterpret_cast<uint4*>(Wk + oRec) : nullptr;
     b.sums = reinterpret_cast<double*>(Wk + oSums);
     lv.map = reinterpret_cast<int*>(K + oMap);
@@ -439,7 +464,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
                              per);
             b.D = lv.sb.D + (size_t)k * per * (dsec / 8);
             launch_dinit(b, per, lv.R0max, sk);
-            int e = launch_hseg_loop(b, per, sk);
+            int e = lv.grid ? launch_grid_loop(b, per, c->nsm, sk, &lv.gridG) : launch_hseg_loop(b, per, sk);
             if (e != cudaSuccess)
                 return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
             c->launches += 3;
@@ -467,7 +492,7 @@ static int run_level(rhseg_ctx* c, Level& lv, cudaStream_t st, const LeafPipe* p
             CK(cudaGetLastError());
             {
                 PhaseTimer t(c, 2, st);
-                int e = launch_hseg_loop(b, n, st);
+                int e = lv.grid ? launch_grid_loop(b, n, c->nsm, st, &lv.gridG) : launch_hseg_loop(b, n, st);
                 c->launches += 1;
                 if (e != cudaSuccess)
                     return fail(RHSEG_E_CUDA, std::string("hseg loop launch: ") + cudaGetErrorString((cudaError_t)e));
@@ -593,7 +618,7 @@ static void finish_phases(rhseg_ctx* c) {
     c->phases_valid = true;
 }
 
-static int validate(const rhseg_params* p, int edge, int bands) {
+static int validate(const rhseg_params* p, int edge, int bands, long long max_regions) {
     if (!p) return fail(RHSEG_E_INVALID, "params is NULL");
     if (!(p->spectral_weight >= 0.0 && p->spectral_weight <= 1.0))
         return fail(RHSEG_E_INVALID, "spectral_weight must be in [0, 1]");
@@ -620,16 +645,17 @@ static int validate(const rhseg_params* p, int edge, int bands) {
         const long long e = edge / side, sect = p->section_target_regions > 0 ? p->section_target_regions
                                                                             : p->target_regions;
         long long R = e * e;
-        if (R > kMaxSectionRegions)
+        if (R > max_regions)
             return fail(RHSEG_E_TOO_LARGE, "leaf sections of " + std::to_string(e) + "x" + std::to_string(e) +
-                                               " pixels exceed " + std::to_string(kMaxSectionRegions) + " regions");
+                                               " pixels exceed " + std::to_string(max_regions) +
+                                               " regions (the dissimilarity matrix would not fit device memory)");
         for (int level = p->levels - 1; level >= 1; --level) {
             R = 4 * std::min(R, sect);
-            if (R > kMaxSectionRegions)
+            if (R > max_regions)
                 return fail(RHSEG_E_TOO_LARGE, "level-" + std::to_string(level) + " sections can hold " +
                                                    std::to_string(R) + " regions (section_target_regions " +
                                                    std::to_string(sect) + "), above the " +
-                                                   std::to_string(kMaxSectionRegions) + "-region section limit");
+                                                   std::to_string(max_regions) + "-region limit of device memory");
         }
     }
     return RHSEG_OK;
@@ -720,7 +746,7 @@ static int ensure_pipeline(rhseg_ctx* c) {
 static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int bands, const rhseg_params* p,
                            int top, int r0, int c0, int nr, int nc, cudaStream_t st,
                            const float* h_samples = nullptr) {
-    int rc = validate(p, edge, bands);
+    int rc = validate(p, edge, bands, c->max_regions);
     if (rc) return rc;
     const int L = p->levels;
     if (top < 1 || top > L) return fail(RHSEG_E_INVALID, "top_level must be in [1, levels]");
@@ -739,8 +765,6 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
     const int sect = p->section_target_regions > 0 ? p->section_target_regions : p->target_regions;
     const int side = 1 << (L - 1);
     const int e = edge / side;
-    if ((long long)e * e > kMaxSectionRegions)
-        return fail(RHSEG_E_TOO_LARGE, "leaf sections above 128x128 pixels are not supported");
     c->levels.reserve(L);
     // ---- leaves ----
     {
@@ -842,6 +866,11 @@ int rhseg_ctx_create(int device, rhseg_ctx** out) {
     rhseg_ctx* c = new rhseg_ctx();
     c->device = device;
     c->nsm = prop.multiProcessorCount;
+    {   // the largest section whose D (R^2 fp64) plus adjacency bitset takes at most 75% of HBM
+        const double per2 = 8.0 + 1.0 / 8.0;
+        long long r = (long long)std::sqrt(0.75 * (double)prop.totalGlobalMem / per2);
+        c->max_regions = std::max<long long>(kMaxSectionRegions, r / 64 * 64);
+    }
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t thr = UINT64_MAX;
@@ -943,7 +972,7 @@ int rhseg_export_top(rhseg_ctx* c, int32_t rp, void* d_pack, void* stream) {
 int rhseg_run_upper(rhseg_ctx* c, const void* d_pack, int32_t top_level, int32_t rp, const int32_t* R0,
                     const int32_t* nlog, int32_t edge, int32_t bands, const rhseg_params* p, void* stream) {
     if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
-    int rc = validate(p, edge, bands);
+    int rc = validate(p, edge, bands, c->max_regions);
     if (rc) return rc;
     if (top_level < 2 || top_level > p->levels) return fail(RHSEG_E_INVALID, "top_level must be in [2, levels]");
     if (rp < 32 || rp % 32) return fail(RHSEG_E_INVALID, "rp must be a positive multiple of 32");
@@ -1025,13 +1054,14 @@ int rhseg_result_level_info(rhseg_ctx* c, int32_t level, int32_t* nsec, int32_t*
         if (lv.imported || lv.level != level) continue;
         if (nsec) *nsec = lv.nsec;
         if (rp) *rp = lv.Rp;
-        if (cluster) *cluster = lv.C;
+        if (cluster) *cluster = lv.grid ? lv.gridG : lv.C;
         if (loop_variant) {
             static const bool recut = [] {
                 const char* e = getenv("RHSEG_APO_V2");
                 return e && e[0] == '1';
             }();
-            *loop_variant = !lv.sb.spec ? RHSEG_LOOP_ADJACENT
+            *loop_variant = lv.grid ? RHSEG_LOOP_GRID
+                            : !lv.sb.spec ? RHSEG_LOOP_ADJACENT
                             : lv.sb.apo ? (recut ? RHSEG_LOOP_APO_RECUT : RHSEG_LOOP_APO)
                                         : RHSEG_LOOP_STREAM;
         }
@@ -1190,7 +1220,7 @@ int rhseg_run_host(rhseg_ctx* c, const float* h_samples, int32_t edge, int32_t b
                    void* stream, int32_t* log_survivor, int32_t* log_absorbed, double* log_dissim,
                    uint8_t* log_kind, int32_t* labels, rhseg_result_info* info) {
     if (!c) return fail(RHSEG_E_INVALID, "ctx is NULL");
-    int rc = validate(p, edge, bands);
+    int rc = validate(p, edge, bands, c->max_regions);
     if (rc) return rc;
     CK(cudaSetDevice(c->device));
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : c->stream;
@@ -1230,8 +1260,9 @@ int rhseg_hseg_graph(rhseg_ctx* c, int64_t n, int64_t nbands, const double* coun
         return fail(RHSEG_E_INVALID, "unknown measure; available: ['euclidean', 'sam', 'sqrt-bsmse']");
     if (target < 1) return fail(RHSEG_E_INVALID, "target_regions must be >= 1");
     if (n < 0 || nbands < 1) return fail(RHSEG_E_INVALID, "bad graph shape");
-    if (n > kMaxSectionRegions)
-        return fail(RHSEG_E_TOO_LARGE, "graph exceeds " + std::to_string(kMaxSectionRegions) + " regions");
+    if (n > c->max_regions)
+        return fail(RHSEG_E_TOO_LARGE, "graph of " + std::to_string(n) + " regions: its dissimilarity matrix " +
+                                           "exceeds device memory (max " + std::to_string(c->max_regions) + ")");
     CK(cudaSetDevice(c->device));
     cudaStream_t st = c->stream;
     reset_ctx(c, st);

@@ -63,12 +63,39 @@ struct SectionBatch {
     long long* nresc;    // [nsec] rows rescanned from D by the merge loop (traffic accounting)
     int sec0;            // first section covered by D (D is allocated per launch chunk)
     unsigned long long* prof;  // [5] per-phase cycles summed over CTAs (nullptr = off)
+    int G;               // grid loop (grid_loop.cu): CTAs per section (0 = cluster/CTA loops)
+    void* gscr;          // grid loop: per-section scratch (group barrier, slots, pending, live bits)
 
     __host__ __device__ size_t mu_stride() const { return (size_t)B * Rp; }
     __host__ __device__ size_t d_stride() const { return (size_t)Rp * Rp; }
     __host__ __device__ size_t sums_copy() const { return (size_t)Rp * B; }
     __host__ __device__ size_t adj_copy() const { return (size_t)Rp * W; }
 };
+
+// Per-section scratch of the grid loop (grid_loop.cu), G CTAs per section; every CTA's
+// slot is written to kGridSlotRep replicas (128 bytes each, flag-carrying words).
+constexpr int kGridSlotRep = 16;
+struct GridScrLayout {
+    size_t bar, slots, pend, pend_each, live, acc, bytes;
+};
+__host__ __device__ inline GridScrLayout grid_scr_layout(int G, int B, int W) {
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    GridScrLayout L;
+    size_t o = 0;
+    L.bar = o;
+    o += 256;
+    L.slots = o;
+    o += al((size_t)2 * kGridSlotRep * G * 128);
+    L.pend_each = al(16 + (size_t)8 * B);
+    L.pend = o;
+    o += 2 * L.pend_each;
+    L.live = o;
+    o += al((size_t)4 * W);
+    L.acc = o;
+    o += 256;
+    L.bytes = o;
+    return L;
+}
 
 // Kernel launchers (hseg_kernels.cu / section_kernels.cu). All stream-ordered.
 void launch_dinit(const SectionBatch& b, int nrun, int R0max, cudaStream_t st);
@@ -77,6 +104,8 @@ int launch_apo_loop(const SectionBatch& b, int nrun, cudaStream_t st);   // apo_
 size_t apo_loop_smem(int Rp, int B);
 int launch_adj_loop(const SectionBatch& b, int nrun, int nsm, cudaStream_t st);   // adj_loop.cu (w = 0, C = 1)
 size_t adj_loop_smem(int Rp, int B, int nwarps);
+int launch_grid_loop(const SectionBatch& b, int nrun, int nsm, cudaStream_t st, int* G_used);  // grid_loop.cu
+size_t grid_loop_scratch_bytes(int nsm, int B, int W);                            // per section
 size_t hseg_loop_smem(int Rp, int C, int B, bool spec, int measure, int stage_bytes, int nstages);
 int hseg_loop_max_stages();
 int hseg_loop_default_stages();

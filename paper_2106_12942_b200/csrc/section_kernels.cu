@@ -158,7 +158,7 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
             int tot;
             const int pre = block_excl_scan(live, scratch, tot);
             if (i < R0c) map[i] = live ? base + pre : -1;
-            if (live) pparent[base + pre] = (k << 16) | i;
+            if (live) pparent[base + pre] = (k << 24) | i;
             base += tot;
         }
     }
@@ -167,7 +167,7 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
     const int R = base;  // == pa.R0[P]
     for (int idx = threadIdx.x; idx < R * B; idx += kThreads) {
         const int m = idx / B, q = idx - m * B;
-        const int src = pparent[m], k = src >> 16, i = src & 0xffff, c = cidx[k];
+        const int src = pparent[m], k = src >> 24, i = src & 0xffffff, c = cidx[k];
         const double cn = (double)ch.count[(size_t)c * ch.Rp + i];
         if (q == 0) pcnt[m] = ch.count[(size_t)c * ch.Rp + i];
         const double s = ch.sums[(size_t)c * ch.C * ch.sums_copy() + (size_t)i * B + q];  // copy 0
@@ -177,7 +177,7 @@ stitch_kernel(SectionBatch ch, int ccols, SectionBatch pa, int pcols, int* cmap,
     }
     for (int idx = threadIdx.x; idx < R * ch.W; idx += kThreads) {
         const int m = idx / ch.W, w = idx - m * ch.W;
-        const int src = pparent[m], k = src >> 16, i = src & 0xffff, c = cidx[k];
+        const int src = pparent[m], k = src >> 24, i = src & 0xffffff, c = cidx[k];
         uint32_t bits = ch.adj[(size_t)c * ch.C * ch.adj_copy() + (size_t)i * ch.W + w];  // copy 0
         const int* map = cmap + (size_t)c * ch.Rp;
         while (bits) {
