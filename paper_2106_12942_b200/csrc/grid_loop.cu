@@ -43,7 +43,11 @@
 
 namespace rhseg {
 
-constexpr int kGT = 512;  // threads per CTA: one CTA per SM
+#ifndef RHSEG_GRID_THREADS
+#define RHSEG_GRID_THREADS 256  // C1 on the grid loop: 73.4 ms at 512, 69.8 ms at 256 threads
+#endif
+constexpr int kGT = RHSEG_GRID_THREADS;  // threads per CTA: one CTA per SM
+constexpr int kMaxGridCTAs = 160;         // CTAs per section (>= the SM count)
 #ifndef RHSEG_GRID_BACKOFF_NS
 #define RHSEG_GRID_BACKOFF_NS 64  // slot polling back-off
 #endif
@@ -139,29 +143,73 @@ __device__ __forceinline__ void cache_offer_g(double& cd, int& cj, double d, int
     }
 }
 
-// Block-wide minima of two pairs and two row bests in one shared exchange.
+// Block-wide minima of two pairs and two row bests in one shared exchange: warp minima,
+// then every warp reduces the kGW per-warp entries with a 5-level butterfly (no serial
+// per-thread pass over the entries: that tail dominated the kernel's instruction count).
+__device__ __forceinline__ void gslot_min(GSlot& v, const GSlot& c) {
+    if (pair_less(c.selA, v.selA)) v.selA = c.selA;
+    if (pair_less(c.selN, v.selN)) v.selN = c.selN;
+    v.rpA = rb_min(v.rpA, c.rpA);
+    v.rpN = rb_min(v.rpN, c.rpN);
+}
+__device__ __forceinline__ GSlot gslot_shfl(const GSlot& v, int o) {
+    GSlot c;
+    c.selA.d = __shfl_xor_sync(0xffffffffu, v.selA.d, o);
+    c.selA.lo = __shfl_xor_sync(0xffffffffu, v.selA.lo, o);
+    c.selA.hi = __shfl_xor_sync(0xffffffffu, v.selA.hi, o);
+    c.selN.d = __shfl_xor_sync(0xffffffffu, v.selN.d, o);
+    c.selN.lo = __shfl_xor_sync(0xffffffffu, v.selN.lo, o);
+    c.selN.hi = __shfl_xor_sync(0xffffffffu, v.selN.hi, o);
+    c.rpA.d = __shfl_xor_sync(0xffffffffu, v.rpA.d, o);
+    c.rpA.j = __shfl_xor_sync(0xffffffffu, v.rpA.j, o);
+    c.rpN.d = __shfl_xor_sync(0xffffffffu, v.rpN.d, o);
+    c.rpN.j = __shfl_xor_sync(0xffffffffu, v.rpN.j, o);
+    return c;
+}
+__device__ __forceinline__ GSlot gslot_none() { return GSlot{pair_none(), pair_none(), rb_none(), rb_none()}; }
 __device__ __forceinline__ void block_min4(Pair& pa, Pair& pn, RowBest& ra, RowBest& rn, GSlot* scr) {
-    pa = warp_min_pair(pa);
-    pn = warp_min_pair(pn);
-    ra = warp_min_rb(ra);
-    rn = warp_min_rb(rn);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) scr[warp] = GSlot{pa, pn, ra, rn};
-    __syncthreads();
-    GSlot r = scr[0];
+    GSlot v{pa, pn, ra, rn};
 #pragma unroll
-    for (int w = 1; w < kGW; ++w) {
-        const GSlot& s = scr[w];
-        if (pair_less(s.selA, r.selA)) r.selA = s.selA;
-        if (pair_less(s.selN, r.selN)) r.selN = s.selN;
-        r.rpA = rb_min(r.rpA, s.rpA);
-        r.rpN = rb_min(r.rpN, s.rpN);
+    for (int o = 16; o > 0; o >>= 1) gslot_min(v, gslot_shfl(v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) scr[warp] = v;
+    __syncthreads();
+    v = lane < kGW ? scr[lane] : gslot_none();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gslot_min(v, gslot_shfl(v, o));
+    __syncthreads();
+    pa = v.selA;
+    pn = v.selN;
+    ra = v.rpA;
+    rn = v.rpN;
+}
+// The same for two row bests only (the rescans).
+__device__ __forceinline__ void block_min2rb(RowBest& ra, RowBest& rn, GSlot* scr) {
+    auto sh = [](RowBest& x, int o) {
+        RowBest c;
+        c.d = __shfl_xor_sync(0xffffffffu, x.d, o);
+        c.j = __shfl_xor_sync(0xffffffffu, x.j, o);
+        x = rb_min(x, c);
+    };
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sh(ra, o);
+        sh(rn, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        scr[warp].rpA = ra;
+        scr[warp].rpN = rn;
     }
     __syncthreads();
-    pa = r.selA;
-    pn = r.selN;
-    ra = r.rpA;
-    rn = r.rpN;
+    ra = lane < kGW ? scr[lane].rpA : rb_none();
+    rn = lane < kGW ? scr[lane].rpN : rb_none();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        sh(ra, o);
+        sh(rn, o);
+    }
+    __syncthreads();
 }
 
 // dynamic shared memory: caches and counts of up to `rows` own rows, m' [B], the rescan
@@ -246,8 +294,7 @@ __device__ __forceinline__ void rescan_row(int i, int which, int skip, const dou
             }
         }
     }
-    Pair dummyA = pair_none(), dummyN = pair_none();
-    block_min4(dummyA, dummyN, bA, bN, scr);
+    block_min2rb(bA, bN, scr);
     oA = bA;
     oN = bN;
 }
@@ -305,10 +352,10 @@ __global__ void __launch_bounds__(kGT, 1) hseg_grid_kernel(SectionBatch bt) {
     auto collect = [&](unsigned seq, Pair& sA, Pair& sN, RowBest& rA, RowBest& rN) {
         const int par = (int)((seq - 1) & 1);
         const unsigned long long* base = slots + (size_t)(par * kGridSlotRep + rep_me) * G * 16;
-        // this thread's words (G * 16 <= 148 * 16 < 5 * kGT), all polls in flight at once,
-        // a short back-off between rounds so the spinning does not crowd out the step's
-        // own L2 traffic
-        constexpr int K = 5;
+        // this thread's words (G * 16 <= K * kGT), all polls in flight at once, a short
+        // back-off between rounds so the spinning does not crowd out the step's own L2
+        // traffic
+        constexpr int K = (kMaxGridCTAs * 16 + kGT - 1) / kGT;
         uint32_t pend = 0u;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -639,7 +686,7 @@ static void* pick_grid_kernel(bool spec, int measure) {
 
 int grid_loop_resident(int nsm) {
     // one CTA per SM by construction (__launch_bounds__(kGT, 1), <= ~60 KB of shared memory)
-    return nsm;
+    return std::min(nsm, kMaxGridCTAs);
 }
 
 int launch_grid_loop(const SectionBatch& b0, int nrun, int nsm, cudaStream_t st, int* G_used) {

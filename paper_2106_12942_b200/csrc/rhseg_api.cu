@@ -252,8 +252,11 @@ static int choose_cluster(const rhseg_ctx* c, int nsec, int R0max, int forced, b
 }
 
 // Allocate and zero one level's device state. R0h/tgth must be filled.
-// Grid loop selection: RHSEG_GRID=1 runs every multi-CTA (cluster) section on the grid
-// loop, RHSEG_GRID=0 only the sections a cluster cannot hold.
+// Grid loop selection: sections a cluster cannot hold, and a level that is ONE
+// multi-CTA section (the whole GPU for it: C1's 4096-region HSEG, 88.6 ms on a 16-CTA
+// cluster -> 69.8 ms); RHSEG_GRID=1 also every other multi-CTA section, RHSEG_GRID=0 only
+// the sections a cluster cannot hold. A forced cluster size (rhseg_params.cluster) keeps
+// the cluster loop.
 static int grid_env() {
     static const int v = [] {
         const char* e = getenv("RHSEG_GRID");
@@ -286,7 +289,8 @@ static int alloc_level(rhseg_ctx* c, Level& lv, double weight, cudaStream_t st, 
     // grow the cluster until the per-CTA row slice fits shared memory; sections no
     // cluster holds (or every cluster section under RHSEG_GRID=1) run on the grid loop
     while (lv.C < kMaxCluster && !fits(lv.C)) lv.C *= 2;
-    lv.grid = !fits(lv.C) || lv.R0max > kMaxSectionRegions || (grid_env() == 1 && lv.C > 1);
+    lv.grid = !fits(lv.C) || lv.R0max > kMaxSectionRegions || (grid_env() == 1 && lv.C > 1) ||
+              (grid_env() != 0 && forced_C <= 0 && lv.C > 1 && lv.nsec == 1);
     if (lv.grid) lv.C = 1;
     // stream ring geometry (runtime knobs). Deeper (4 x 32 KB) or bigger (2 x 96 KB)
     // rings for levels with at most one CTA per SM were both measured slower on C2
