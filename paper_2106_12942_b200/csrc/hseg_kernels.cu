@@ -649,6 +649,12 @@ struct StreamState {
 #ifndef RHSEG_KEY32
 #define RHSEG_KEY32 1  // APO rescans on 32-bit keys with redux.sync (0: 64-bit keys, shuffle trees)
 #endif
+#ifndef RHSEG_N_NODEP
+#define RHSEG_N_NODEP 1  // APO non-adjacent-only rescans: D loads independent of the adjacency words
+#endif
+#ifndef RHSEG_ADJ_GATHER
+#define RHSEG_ADJ_GATHER 1  // APO adjacent-only rescans: gather the adjacent columns' D entries only
+#endif
 #ifndef RHSEG_RESCAN_U
 #define RHSEG_RESCAN_U 4  // APO rescans: D loads in flight per lane (C4 loop: 8 -> 427 ms, 4 -> 380, 2 -> 402, 1 -> 387)
 #endif
@@ -1023,6 +1029,50 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     else n2 = min(n2, kn);
                 }
             };
+            if (MK == 1 && RHSEG_ADJ_GATHER && nparts == 1 && W <= 64 && !areg) {
+                // adjacent-only rescan: the row's adjacency words in one coalesced load,
+                // then the D entries of the (few) adjacent live columns only -- two rounds
+                // of loads instead of a dependent (adjacency word, D) pair per batch of words
+                uint32_t w0 = lane < W ? arow[lane] & livew[lane] : 0u;
+                uint32_t w1 = 32 + lane < W ? arow[32 + lane] & livew[32 + lane] : 0u;
+                auto clr = [&](int j) {
+                    if (j < 0) return;
+                    if ((j >> 5) == lane) w0 &= ~(1u << (j & 31));
+                    if ((j >> 5) == 32 + lane) w1 &= ~(1u << (j & 31));
+                };
+                clr(i);
+                clr(ex);
+                clr(rs_exb);
+                const int cb = __popc(w0) + __popc(w1);
+                int incl = cb;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                if (tot <= 2 * B) {  // (uniform) the list fits this warp's staging row
+                    int* lst = reinterpret_cast<int*>(xstg);
+                    int k = incl - cb;
+                    for (uint32_t m = w0; m; m &= m - 1) lst[k++] = (lane << 5) + __ffs(m) - 1;
+                    for (uint32_t m = w1; m; m &= m - 1) lst[k++] = ((32 + lane) << 5) + __ffs(m) - 1;
+                    __syncwarp();
+                    for (int t0 = 0; t0 < tot; t0 += 32 * U) {
+                        double dv[U];
+                        int jv[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int t = t0 + 32 * u + lane;
+                            jv[u] = t < tot ? lst[t] : -1;
+                            dv[u] = jv[u] >= 0 ? __ldcs(drow + jv[u]) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) take(dv[u], jv[u], jv[u] >= 0, true);
+                    }
+                    __syncwarp();  // (the staging row is the exact fallback's next)
+                    return;
+                }
+            }
             if (RHSEG_SPARSE_DEN * ss.S < RHSEG_SPARSE_NUM * R0) {
                 // sparse (most regions merged away): walk the compacted live-column list
                 const int slo = part * ss.S / nparts, shi = (part + 1) * ss.S / nparts;
@@ -1059,9 +1109,13 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         const uint32_t lw = w < whi ? livew[w] : 0u, aw = w < whi ? aword(w) : 0u;
                         const int j = (w << 5) + lane;
                         const bool aj = (aw >> lane) & 1u;
-                        const bool c = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb && (aj ? (MK & 1) : (MK & 2));
+                        const bool lv = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb;
+                        const bool c = lv && (aj ? (MK & 1) : (MK & 2));
                         sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
-                        dv[u] = c ? (sbuf ? sbuf[j] : __ldcs(drow + j)) : 0.0;
+                        // non-adjacent-only walks load every live column's entry, so the D
+                        // load does not wait on the adjacency word (c masks the adjacent ones)
+                        const bool ld = (MK == 2 && RHSEG_N_NODEP) ? lv : c;
+                        dv[u] = ld ? (sbuf ? sbuf[j] : __ldcs(drow + j)) : 0.0;
                     }
                 };
                 if (RHSEG_RESCAN_PIPE) {
