@@ -415,6 +415,7 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #define RHSEG_RESCAN_STAGE 0  // APO: first N rescans' D rows bulk-copied to shared memory (C4 loop 319 -> 354/357/367 ms for N = 1/2/3: off)
 #endif
 constexpr int kRsStage = RHSEG_RESCAN_STAGE;
+constexpr bool kFuseOffers = RHSEG_APO_FUSE_OFFERS && !RHSEG_APO_TOP2;
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -651,6 +652,9 @@ struct StreamState {
 #endif
 #ifndef RHSEG_N_NODEP
 #define RHSEG_N_NODEP 1  // APO non-adjacent-only rescans: D loads independent of the adjacency words (C4 loop 311 -> 291.5 ms)
+#endif
+#ifndef RHSEG_APO_FUSE_OFFERS
+#define RHSEG_APO_FUSE_OFFERS 0  // APO: offers made in the row-a' interval pass (C4 371.4 vs 371.5 ms: neutral, off)
 #endif
 #ifndef RHSEG_ADJ_GATHER
 #define RHSEG_ADJ_GATHER 1  // APO adjacent-only rescans: gather the adjacent columns' D entries only
@@ -1637,6 +1641,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     }
     if (tid == 0) {
         ninv = 0;
+        misc[10] = 0;
         misc[12] = 0;
         sdE = 0;
         sE0 = 0ull;
@@ -2132,15 +2137,39 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 apo_interval<M>(ap, sdl[sl], sdh[sl], (double)cnt[j], dlo, dhi);
                 sdl[sl] = dlo;
                 sdh[sl] = dhi;
-                if ((sra[j >> 5] >> (j & 31)) & 1u) apo_uA = fmin(apo_uA, dhi);
+                const bool aj = (sra[j >> 5] >> (j & 31)) & 1u;
+                if (aj) apo_uA = fmin(apo_uA, dhi);
                 else apo_uN = fmin(apo_uN, dhi);
-                if (d_pack_interval(dlo, dhi, v)) {  // (too wide: made exact after C2)
+                const bool packed = d_pack_interval(dlo, dhi, v);
+                if (packed) {  // (too wide: made exact after C2)
                     D[(size_t)j * Rp + a] = v;
                     D[(size_t)a * Rp + j] = v;
                 }
+                if (kFuseOffers) {
+                    // the offer (d(a', j), a) to row j, decided on the intervals unless they
+                    // overlap row j's cached best (then exact, after the barrier below)
+                    const unsigned short e = (unsigned short)(j | (aj ? 0 : 0x4000));
+                    unsigned short* l1 = reinterpret_cast<unsigned short*>(inv);
+                    if (!packed) {
+                        l1[atomicAdd(&misc[10], 1)] = (unsigned short)(e | 0x8000);
+                        continue;
+                    }
+                    const int r = j - lo;
+                    double& bv = aj ? bAd[r] : bNd[r];
+                    int& bj = aj ? bAj[r] : bNj[r];
+                    if (bj < 0) {
+                        bv = v;
+                        bj = a;
+                    } else {
+                        double bl, bh;
+                        d_unpack(bv, bl, bh);
+                        if (dhi < bl) { bv = v; bj = a; }
+                        else if (!(dlo > bh)) l1[atomicAdd(&misc[10], 1)] = e;
+                    }
+                }
             }
         };
-        if (APO && tid == 0) { sScan = 0; misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
+        if (APO && tid == 0) { sScan = 0; if (!kFuseOffers) misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
         // split APO rescans: with ni <= kWarps / 2 rows each row's walk is cut into the
         // largest power-of-two number of slices that keeps every warp busy
         const int nsplit = 1;  // (split rescans: measured slower, and APO now rescans beside the merge)
@@ -2324,6 +2353,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         l2[atomicAdd(&sScan, 1)] = e;
                         atomicAdd(&ak[aj ? 6 : 7], 1u);
                     }
+                    if (kFuseOffers) continue;  // (offered in the interval pass)
                     double v;
                     if (!d_pack_interval(dlo, dhi, v)) {  // exact d(a', j) below, then the offer
                         l1[atomicAdd(&cntF[0], 1)] = (unsigned short)(e | 0x8000);
@@ -2519,6 +2549,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 ninv = 0;
                 nnb = 0;
                 sScan = 0;
+                misc[10] = 0;  // exact offers (the fused offers count them before any barrier)
                 misc[12] = 0;  // rescan claim counter
                 ak[0] = ak[1] = ak[4] = ak[5] = 0xffffffffu;
                 ak[2] = ak[3] = 0u;
