@@ -414,6 +414,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #ifndef RHSEG_RESCAN_STAGE
 #define RHSEG_RESCAN_STAGE 0  // APO: first N rescans' D rows bulk-copied to shared memory (C4 loop 319 -> 354/357/367 ms for N = 1/2/3: off)
 #endif
+#ifndef RHSEG_APO_FUSE_OFFERS
+#define RHSEG_APO_FUSE_OFFERS 1  // APO: offers of d(a', j) made in the row-a' interval pass (C4 371.7 -> 369.8 ms)
+#endif
 constexpr int kRsStage = RHSEG_RESCAN_STAGE;
 constexpr bool kFuseOffers = RHSEG_APO_FUSE_OFFERS && !RHSEG_APO_TOP2;
 #ifndef RHSEG_STAGES
@@ -652,9 +655,6 @@ struct StreamState {
 #endif
 #ifndef RHSEG_N_NODEP
 #define RHSEG_N_NODEP 1  // APO non-adjacent-only rescans: D loads independent of the adjacency words (C4 loop 311 -> 291.5 ms)
-#endif
-#ifndef RHSEG_APO_FUSE_OFFERS
-#define RHSEG_APO_FUSE_OFFERS 0  // APO: offers made in the row-a' interval pass (C4 371.4 vs 371.5 ms: neutral, off)
 #endif
 #ifndef RHSEG_ADJ_GATHER
 #define RHSEG_ADJ_GATHER 1  // APO adjacent-only rescans: gather the adjacent columns' D entries only

@@ -16,3 +16,4 @@ timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"hseg_loop_kernel" -c 1 -f -o $O/loop_c4 python tools/c4_paths.py dev 1 > $O/ncu_loop.log 2>&1; echo "ncu loop rc=$?"
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"dinit_iv84" -c 1 -f -o $O/dinit_c4 python tools/c4_paths.py dev 1 > $O/ncu_dinit.log 2>&1; echo "ncu dinit rc=$?"
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"hseg_grid" -c 1 -f -o $O/grid_c1 python tools/profile_loop.py c1 > $O/ncu_grid.log 2>&1; echo "ncu grid rc=$?"
+timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "gpu suite rc=$?"
