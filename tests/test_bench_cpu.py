@@ -58,3 +58,14 @@ def test_loop_variant_names_follow_the_abi():
     assert set(codes.values()) == set(_lib.LOOP_NAMES)
     assert _lib.LOOP_NAMES[codes["RHSEG_LOOP_APO"]] == "APO"
     assert _lib.LOOP_NAMES[codes["RHSEG_LOOP_ADJACENT"]].startswith("adjacent")
+    assert _lib.LOOP_NAMES[codes["RHSEG_LOOP_GRID"]] == "grid"
+
+
+def test_grid_loop_sections_have_no_fixed_region_limit():
+    """The 16384-region section limit is gone from the drop-in contract (sections above a
+    cluster's capacity run on the grid loop); only device memory for D bounds a section."""
+    hdr = open(os.path.join(ROOT, "include", "rhseg_b200.h")).read()
+    m = re.search(r"#define RHSEG_E_TOO_LARGE \d+\s*/\*(.*?)\*/", hdr)
+    assert m and "16384" not in m.group(1) and "memory" in m.group(1)
+    api = open(os.path.join(ROOT, "paper_2106_12942_b200", "csrc", "rhseg_api.cu")).read()
+    assert "launch_grid_loop" in api and "max_regions" in api
