@@ -790,7 +790,14 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
         rc = alloc_level(c, lv, p->spectral_weight, st, p->cluster, 0);
         RHSEG_TRACE("leaves: alloc done");
         if (rc) return rc;
-        const bool piped = h_samples && L >= 2 && top == 1;
+        // RHSEG_DEV_PIPE=1: the device-resident path runs the leaf level in the same chunks
+        // on concurrent streams (the FP64-bound all-pairs init of one chunk beside the
+        // latency-bound merge loops of the others)
+        static const bool dev_pipe = [] {
+            const char* e = getenv("RHSEG_DEV_PIPE");
+            return e && e[0] == '1';
+        }();
+        const bool piped = (h_samples || dev_pipe) && L >= 2 && top == 1;
         if (piped) {
             // upload in K bands of leaf rows on the copy stream; chunk k starts as soon
             // as its rows land (run_level / LeafPipe)
@@ -800,9 +807,13 @@ static int run_device_impl(rhseg_ctx* c, const float* d_samples, int edge, int b
             const size_t rows = (size_t)edge / pipe.K, plane = (size_t)edge * edge;
             for (int k = 0; k < pipe.K; ++k) {
                 const size_t off = (size_t)k * rows * edge;
-                CK(cudaMemcpy2DAsync(const_cast<float*>(d_samples) + off, plane * 4, h_samples + off, plane * 4,
-                                     rows * edge * 4, (size_t)bands, cudaMemcpyHostToDevice, c->copy_stream));
-                CK(cudaEventRecord(c->ready[k], c->copy_stream));
+                if (h_samples) {
+                    CK(cudaMemcpy2DAsync(const_cast<float*>(d_samples) + off, plane * 4, h_samples + off, plane * 4,
+                                         rows * edge * 4, (size_t)bands, cudaMemcpyHostToDevice, c->copy_stream));
+                    CK(cudaEventRecord(c->ready[k], c->copy_stream));
+                } else {
+                    CK(cudaEventRecord(c->ready[k], st));  // (resident: ready now)
+                }
             }
             rc = run_level(c, lv, st, &pipe);
             if (rc) return rc;
