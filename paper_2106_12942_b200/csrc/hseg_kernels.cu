@@ -419,6 +419,9 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #endif
 constexpr int kRsStage = RHSEG_RESCAN_STAGE;
 constexpr bool kFuseOffers = RHSEG_APO_FUSE_OFFERS && !RHSEG_APO_TOP2;
+#ifndef RHSEG_RESCAN_LPT
+#define RHSEG_RESCAN_LPT 1  // APO: rescans claimed longest first (full walks, then adjacent-only gathers)
+#endif
 #ifndef RHSEG_STAGES
 #define RHSEG_STAGES 2
 #endif
@@ -690,6 +693,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     // candidate" bit (the SAM lists, on intervals): a merge removes a and b from every
     // list and only a list left empty and incomplete is rescanned
     constexpr bool T2A = APO && RHSEG_APO_TOP2;
+    constexpr bool kLpt = APO && !T2A && RHSEG_RESCAN_LPT;  // (rescan claim order, see the claim loop)
     constexpr bool STREAM = SPEC && !APO;  // row a' from the streamed mean columns
     using SE = double;  // streamed element
     constexpr int ES = (int)sizeof(SE);
@@ -1641,6 +1645,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
     }
     if (tid == 0) {
         ninv = 0;
+        misc[14] = 0;
         misc[10] = 0;
         misc[12] = 0;
         sdE = 0;
@@ -1952,7 +1957,8 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 if (SPEC && (bNj[r] == a || bNj[r] == b)) mask |= 2;
             }
             if (mask) {
-                inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
+                if (kLpt && mask == 1) inv[Rs - 1 - atomicAdd(&misc[14], 1)] = (i << 2) | mask;  // cheap: last
+                else inv[atomicAdd(&ninv, 1)] = (i << 2) | mask;
                 // its D row is read by the rescan after the merge: start the fetch now
                 if (RHSEG_RESCAN_PREFETCH) bulk_prefetch_l2(D + (size_t)i * Rp, (uint32_t)(((R0 + 1) & ~1) * 8));
             }
@@ -2049,17 +2055,20 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             // the rescans: rows claimed from a shared counter (the merge warps join when done)
             const long long tr0 = clock64();
             int nr = 0;
-            const int ni = ninv;
+            // full walks first, adjacent-only gathers (a few loads) last: the slowest warp
+            // sets the step, so the long items go out first (LPT)
+            const int nf = ninv, ni = nf + (kLpt ? misc[14] : 0);
             for (;;) {
                 int k = 0;
                 if (lane == 0) k = atomicAdd(&misc[12], 1);
                 k = __shfl_sync(0xffffffffu, k, 0);
                 if (k >= ni) break;
+                const int e = k < nf ? inv[k] : inv[Rs - 1 - (k - nf)];
                 if (kRsStage && k < kRsStage) {
                     mbar_wait(&bars[k], (rbph_now >> k) & 1u);
-                    rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0, rbuf + (size_t)k * Rp);
+                    rescanf(e >> 2, e & 3, a, 0, 1, 0, rbuf + (size_t)k * Rp);
                 } else {
-                    rescanf(inv[k] >> 2, inv[k] & 3, a, 0, 1, 0);
+                    rescanf(e >> 2, e & 3, a, 0, 1, 0);
                 }
                 ++nr;
             }
@@ -2547,6 +2556,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     cx[r] = (uint8_t)((pA.j == kNoJ ? 1 : 0) | (pN.j == kNoJ ? 2 : 0));
                 }
                 ninv = 0;
+                misc[14] = 0;
                 nnb = 0;
                 sScan = 0;
                 misc[10] = 0;  // exact offers (the fused offers count them before any barrier)
