@@ -419,6 +419,12 @@ static_assert(sizeof(Slot) == 64, "slot is copied as 16 u32 words");
 #endif
 constexpr int kRsStage = RHSEG_RESCAN_STAGE;
 constexpr bool kFuseOffers = RHSEG_APO_FUSE_OFFERS && !RHSEG_APO_TOP2;
+#ifndef RHSEG_RESCAN_HI
+#define RHSEG_RESCAN_HI 0  // APO rescans on the high words of D, 2U loads in flight (C4 372.6 -> 411.7 ms: off)
+#endif
+#ifndef RHSEG_RESCAN_HI_KMAX
+#define RHSEG_RESCAN_HI_KMAX 24  // ... while every interval code in D is at most this (else full doubles)
+#endif
 #ifndef RHSEG_RESCAN_LPT
 #define RHSEG_RESCAN_LPT 1  // APO: rescans claimed longest first (full walks, then adjacent-only gathers)
 #endif
@@ -1003,6 +1009,13 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         double va = kInf, vn = kInf;
         int km = 0;  // widest interval code over both stages (only widens the test)
         constexpr int U = RHSEG_RESCAN_U;
+        // high-word walk: the keys are the high words of the D bits, so a walk can load 32
+        // bits per entry (twice the entries in flight for the same registers); the
+        // winner's full entry is reloaded afterwards and the interval width bound comes
+        // from the section-wide maximum code (misc[15], every interval ever written to D)
+        const int kms = misc[15];
+        const bool hi_ok = RHSEG_RESCAN_HI && kRsStage == 0 && !sbuf && nparts == 1 && kms <= RHSEG_RESCAN_HI_KMAX;
+        bool hi_used = false;
         // the row's adjacency words (W <= 64 on APO sections), one or two per lane, loaded
         // once: every walk iteration then waits on its D loads only, not on a global
         // adjacency load in front of them (the merges rewrite these rows, so L1 rarely
@@ -1128,7 +1141,42 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                         dv[u] = ld ? (sbuf ? sbuf[j] : __ldcs(drow + j)) : 0.0;
                     }
                 };
-                if (RHSEG_RESCAN_PIPE) {
+                if (hi_ok) {
+                    hi_used = true;
+                    constexpr int UH = 2 * U;
+                    auto take_hi = [&](unsigned hw, int j, bool c, bool aj) {
+                        const unsigned key = c ? (hw & 0x7fffffffu) : ~0u;
+                        if (MK == 1 || MK == 3) {
+                            const unsigned ka = (MK == 1 || aj) ? key : ~0u;
+                            if (ka < a1) { a2 = a1; a1 = ka; ja = j; }
+                            else a2 = min(a2, ka);
+                        }
+                        if (MK == 2 || MK == 3) {
+                            const unsigned kn = (MK == 2 || !aj) ? key : ~0u;
+                            if (kn < n1) { n2 = n1; n1 = kn; jn = j; }
+                            else n2 = min(n2, kn);
+                        }
+                    };
+                    const unsigned* dhw = reinterpret_cast<const unsigned*>(drow) + 1;  // high words
+                    for (int w0 = wlo; w0 < whi; w0 += UH) {
+                        unsigned hv[UH];
+                        uint32_t sel[UH];
+#pragma unroll
+                        for (int u = 0; u < UH; ++u) {
+                            const int w = w0 + u;
+                            const uint32_t lw = w < whi ? livew[w] : 0u, aw = w < whi ? aword(w) : 0u;
+                            const int j = (w << 5) + lane;
+                            const bool aj = (aw >> lane) & 1u;
+                            const bool lv = ((lw >> lane) & 1u) && j != i && j != ex && j != rs_exb;
+                            const bool c = lv && (aj ? (MK & 1) : (MK & 2));
+                            sel[u] = (c ? 1u : 0u) | (aj ? 2u : 0u);
+                            const bool ld = (MK == 2 && RHSEG_N_NODEP) ? lv : c;
+                            hv[u] = ld ? __ldcs(dhw + 2 * j) : 0u;
+                        }
+#pragma unroll
+                        for (int u = 0; u < UH; ++u) take_hi(hv[u], ((w0 + u) << 5) + lane, sel[u] & 1u, sel[u] & 2u);
+                    }
+                } else if (RHSEG_RESCAN_PIPE) {
                     // software-pipelined: the next batch's loads are in flight while this
                     // batch is folded into the keys
                     double dv[U], dn[U];
@@ -1158,7 +1206,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             else walk(std::integral_constant<int, 3>{});
         }
         if (kRsStage && sbuf) fence_proxy_async_shared();  // the buffer's next fill is an async write
-        km = __reduce_max_sync(0xffffffffu, km);
+        km = hi_used ? kms : __reduce_max_sync(0xffffffffu, km);
         // warp minimum of one stage: the smallest key, the second smallest (== the
         // smallest on a tie), the winner's column and D value
         auto reduce = [&](unsigned& k1, unsigned& k2, int& j1, double& v1) {
@@ -1189,14 +1237,14 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
             return;
         }
         int slow = 0;
-        if (mask & 1) {
-            reduce(a1, a2, ja, va);
-            if (a1 != ~0u && !unique32(a2, va)) slow |= 1;
+        if (mask & 1) reduce(a1, a2, ja, va);
+        if (mask & 2) reduce(n1, n2, jn, vn);
+        if (hi_used) {  // the winners' full entries (both in flight at once)
+            if ((mask & 1) && a1 != ~0u) va = __ldcs(drow + ja);
+            if ((mask & 2) && n1 != ~0u) vn = __ldcs(drow + jn);
         }
-        if (mask & 2) {
-            reduce(n1, n2, jn, vn);
-            if (n1 != ~0u && !unique32(n2, vn)) slow |= 2;
-        }
+        if ((mask & 1) && a1 != ~0u && !unique32(a2, va)) slow |= 1;
+        if ((mask & 2) && n1 != ~0u && !unique32(n2, vn)) slow |= 2;
         if (lane == 0) {
             const int r = i - lo;
             if ((mask & 1) && !(slow & 1)) { bAd[r] = a1 == ~0u ? kInf : va; bAj[r] = a1 == ~0u ? -1 : ja; }
@@ -1647,6 +1695,10 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         ninv = 0;
         misc[14] = 0;
         misc[10] = 0;
+        // widest interval code in D so far: the all-pairs init's intervals c (1 -/+ 2^(k-46))
+        // around d (1 -/+ rho), rho = 2 (B + 4) u, need 2^(k-46) >= rho + 2^-45 (truncated
+        // centre); +1 spare. apo_rows raises it with every interval it writes.
+        misc[15] = APO ? 47 + (int)ceil(log2(2.0 * (B + 4) * kU64 + 0x1p-45)) : 0;
         misc[12] = 0;
         sdE = 0;
         sE0 = 0ull;
@@ -2121,6 +2173,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
         auto apo_rows = [&]() {
             double* sdl = reinterpret_cast<double*>(smem + L.sdv);
             double* sdh = sdl + Rs;
+            int kw = 0;  // widest interval code this thread writes to D
             const double* Da = D + (size_t)a * Rp;
             const double* Db = D + (size_t)b * Rp;
             constexpr int NQ = kMaxSlots / kThreads;
@@ -2153,6 +2206,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                 if (packed) {  // (too wide: made exact after C2)
                     D[(size_t)j * Rp + a] = v;
                     D[(size_t)a * Rp + j] = v;
+                    if (RHSEG_RESCAN_HI && d_is_interval(v)) kw = max(kw, (int)(__double2loint(v) & 63));
                 }
                 if (kFuseOffers) {
                     // the offer (d(a', j), a) to row j, decided on the intervals unless they
@@ -2177,6 +2231,7 @@ __global__ void __launch_bounds__(kThreads, APO ? RHSEG_APO_MINBLOCKS : RHSEG_MI
                     }
                 }
             }
+            if (RHSEG_RESCAN_HI && kw > 0) atomicMax(&misc[15], kw);  // (read by the next step's rescans)
         };
         if (APO && tid == 0) { sScan = 0; if (!kFuseOffers) misc[10] = 0; ak[6] = 0u; ak[7] = 0u; }
         // split APO rescans: with ni <= kWarps / 2 rows each row's walk is cut into the
